@@ -1,0 +1,143 @@
+/*
+ * lmkan_b200.h — C-ABI of the B200-native (sm_100a) lmKAN layer forward.
+ *
+ * This is the drop-in boundary for the reference's layer-forward path. The
+ * reference has no FFI: its interface is the inline C++ function
+ *     void lmkan::lmkan_forward(const LmKanLayer&, const Matrix& X, Matrix& Y,
+ *                               std::size_t workers = 0)          (layer.hpp:108-109)
+ * over the types LmKanLayer (layer.hpp:24-61), SigmaGrid / build_grid
+ * (grid.hpp:33-68) and Matrix (matrix.hpp:11-38). The C++ host API in
+ * include/lmkan_b200/lmkan.hpp restates that interface on top of the entry
+ * points below; a foreign-language binding (ctypes) binds
+ * these symbols directly. Plain pointers and sizes only.
+ *
+ * Paths are relative to /root/reference/proj/include/lmkan/.
+ *
+ * Status codes: every entry point returns 0 on success, else one of
+ * LMKAN_B200_E*; lmkan_b200_last_error() gives a thread-local message. The C++
+ * wrapper maps EINVAL to std::invalid_argument with the reference message
+ * format ("lmkan_forward: expected width N, got M", matrix.hpp:40-44) and the
+ * rest to std::runtime_error.
+ */
+#ifndef LMKAN_B200_H
+#define LMKAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMKAN_B200_OK 0
+#define LMKAN_B200_EINVAL 1  /* maps to std::invalid_argument (matrix.hpp:40-44, layer.hpp:71-73, grid.hpp:45-46) */
+#define LMKAN_B200_ECUDA 2   /* CUDA runtime / launch failure */
+#define LMKAN_B200_ENOMEM 3  /* device or pinned-host allocation failed */
+#define LMKAN_B200_ENOSYS 4  /* no sm_100a device / kernel image */
+
+typedef struct lmkan_b200_layer lmkan_b200_layer; /* opaque prepared device layer */
+
+/* Thread-local message for the last failing call on this thread. */
+const char* lmkan_b200_last_error(void);
+/* Library build string (kernel arch, version). */
+const char* lmkan_b200_version(void);
+
+/* ---- grid (host-side, once per layer) ---- */
+
+/* build_grid (grid.hpp:44-68): points[G+1] with ghost points, inv_areas[G*G].
+ * EINVAL when G < 3. */
+int lmkan_b200_build_grid(int G, double* points, double* inv_areas);
+
+/* Cell-locate threshold tables derived from interval_index (grid.hpp:72-75):
+ * t64[k-1] = min{double x : interval_index(x) >= k}, k = 1..G-1, and t32[k-1]
+ * the smallest float >= t64[k-1]. Then interval_index(x) == #{k : x >= t[k]}
+ * for every input, including +-0, +-inf and NaN (-> 0). Either pointer may be
+ * NULL. */
+int lmkan_b200_thresholds(int G, double* t64, float* t32);
+
+/* init_layer's coefficient table (layer.hpp:69-86): P_out[i] = init_scale *
+ * N(0,1) drawn in reference index order from RandomStream(seed,
+ * "lmkan.layer.init") (rng.hpp:19-79: FNV-1a + splitmix64 keyed mt19937_64,
+ * Box-Muller with one cached value). init_scale < 0 selects (n_in/2)^(-1/2)
+ * (layer.hpp:63-65). Host-only; bit-identical to the reference on the same
+ * libstdc++/glibc. P_out holds (G+1)^2 * (n_in/2) * n_out doubles. */
+int lmkan_b200_init_table(int n_in, int n_out, int G, uint64_t seed, double init_scale, double* P_out);
+
+/* ---- prepared layer handle ---- */
+
+/* Replaces constructing/owning an LmKanLayer (layer.hpp:24-61) for the device:
+ * P_host is the reference table, index order [i1][i2][pair][out] with out
+ * fastest (layer.hpp:20-22, 34-45), (G+1)^2 * (n_in/2) * n_out doubles. It is
+ * rounded to fp32 once and re-laid out on `device` as [out_tile][pair][node][OT]
+ * (node = i1*(G+1)+i2). gamma is the lookup-branch weight (layer.hpp:29).
+ * EINVAL if n_in is not a positive even number, n_out <= 0 or G < 3. */
+int lmkan_b200_layer_create(int n_in, int n_out, int G, double gamma, const double* P_host,
+                            int device, lmkan_b200_layer** out);
+/* Same, from an fp32 table in reference layout already resident on `device`
+ * (e.g. generated there); the relayout runs on the device. */
+int lmkan_b200_layer_create_device_f32(int n_in, int n_out, int G, double gamma,
+                                       const float* P_dev, int device, lmkan_b200_layer** out);
+/* Output-sliced layer: keeps only outputs [out_begin, out_end) of the table
+ * (exact, since y_q depends only on column q of P, layer.hpp:128-129). Used to
+ * shard very wide layers over GPUs. P_dev is the FULL reference-layout table. */
+int lmkan_b200_layer_create_device_f32_slice(int n_in, int n_out, int G, double gamma,
+                                             const float* P_dev, int out_begin, int out_end,
+                                             int device, lmkan_b200_layer** out);
+/* Table generated on the device by a counter-based hash normal RNG:
+ * P[i1][i2][pair][out] = scale * N(0,1)(seed, flat reference index), written
+ * straight into the device layout (no host table, no 2x relayout memory). */
+int lmkan_b200_layer_create_random(int n_in, int n_out, int G, double gamma, uint64_t seed,
+                                   double scale, int out_begin, int out_end, int device,
+                                   lmkan_b200_layer** out);
+/* Copy the fp32 device table back in reference layout for pairs
+ * [pair_begin, pair_end) and the layer's local outputs [0, n_out_local):
+ * dst[node][pair - pair_begin][out] as doubles (for oracle checks). */
+int lmkan_b200_layer_read_table(const lmkan_b200_layer* layer, int pair_begin, int pair_end,
+                                double* dst);
+int lmkan_b200_layer_set_gamma(lmkan_b200_layer* layer, double gamma);
+/* Shape query: any pointer may be NULL. n_out is the layer's local width. */
+int lmkan_b200_layer_info(const lmkan_b200_layer* layer, int* n_in, int* n_out, int* G,
+                          int* device, size_t* table_bytes, int* out_tile);
+int lmkan_b200_layer_destroy(lmkan_b200_layer* layer);
+
+/* ---- forward ---- */
+
+/* Device path (asynchronous on `stream`, a cudaStream_t or NULL for the
+ * legacy default stream). X_dev: [rows][n_in] fp32 row-major, Y_dev:
+ * [rows][n_out] fp32 row-major (layer-local n_out). Same semantics as
+ * lmkan_forward (layer.hpp:108-134): y_q = gamma * sum_p f_qp(x_2p, x_2p+1),
+ * cell indices bit-exact, fp32 accumulation in the reference pair order. */
+int lmkan_b200_forward_f32(const lmkan_b200_layer* layer, const float* X_dev, float* Y_dev,
+                           int64_t rows, void* stream);
+/* Same, with fp64 inputs/outputs on the device (cells located in fp64 against
+ * the fp64 thresholds, so indices stay bit-exact for any double X). */
+int lmkan_b200_forward_f64(const lmkan_b200_layer* layer, const double* X_dev, double* Y_dev,
+                           int64_t rows, void* stream);
+/* Drop-in synchronous host paths: X/Y in host memory (pinned or pageable),
+ * copies and kernels pipelined over row chunks on internal streams; returns
+ * when Y is on the host. `workers` is accepted for signature parity with
+ * lmkan_forward's workers argument (threading.hpp:24-28) and ignored. */
+int lmkan_b200_forward_host_f64(const lmkan_b200_layer* layer, const double* X, double* Y,
+                                int64_t rows, size_t workers);
+int lmkan_b200_forward_host_f32(const lmkan_b200_layer* layer, const float* X, float* Y,
+                                int64_t rows, size_t workers);
+
+/* Debug / parity path: the cell-locate stage alone (row_preambles,
+ * layer.hpp:96-101). i1, i2: [rows][pairs] int32; w: [rows][pairs][4] fp32 in
+ * the order {w00, w10, w01, w11}, each the reference fp64 weight rounded to
+ * fp32. All pointers are device pointers. */
+int lmkan_b200_locate_f32(const lmkan_b200_layer* layer, const float* X_dev, int32_t* i1,
+                          int32_t* i2, float* w, int64_t rows, void* stream);
+int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, int32_t* i1,
+                          int32_t* i2, float* w, int64_t rows, void* stream);
+
+/* Tuning / introspection: kernel variant chosen for `rows` (OT = output tile,
+ * RT = rows per thread, NBUF = sheet buffers, rows_per_cta), and the number of
+ * kernel launches one forward issues. */
+int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
+                    int* nbuf, int* rows_per_cta, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMKAN_B200_H */

@@ -1,0 +1,277 @@
+"""B200-native (sm_100a) lmKAN layer forward — Python view of the C-ABI.
+
+The product is the CUDA library ``lib/liblmkan_b200.so`` (sources in
+``csrc/``) behind the C-ABI ``include/lmkan_b200.h`` and the C++ host API
+``include/lmkan_b200/lmkan.hpp``. This module is the thin ctypes view used by
+the tests and ``bench.py``; it mirrors the reference's C++ interface names
+(paths relative to /root/reference/proj/include/lmkan/):
+
+  build_grid(G)                       grid.hpp:44-68
+  init_layer(n_in, n_out, G, seed)    layer.hpp:69-86   (bit-identical table)
+  LmKanLayer                          layer.hpp:24-61
+  lmkan_forward(layer, X, Y, workers) layer.hpp:108-134 (ValueError where the
+                                       reference throws std::invalid_argument)
+
+plus ``Layer``, the prepared device handle that the fast paths use. Device
+tensors are torch CUDA tensors (torch is used for device memory and streams
+only). Nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Tuple
+
+import numpy as np
+
+from ._lib import LIB_PATH, LmkanError, check, lib  # noqa: F401  (fails loudly if the .so is missing)
+
+__all__ = ["SigmaGrid", "build_grid", "thresholds", "init_table", "Layer", "LmKanLayer", "init_layer",
+           "lmkan_forward", "LmkanError", "LIB_PATH", "version"]
+
+
+def _ptr(a) -> C.c_void_p:
+    if a is None:
+        return C.c_void_p(0)
+    if isinstance(a, np.ndarray):
+        return C.c_void_p(a.ctypes.data)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+def version() -> str:
+    return lib.lmkan_b200_version().decode()
+
+
+@dataclass
+class SigmaGrid:
+    """grid.hpp:33-39: G intervals, points[G+1] (ghost ends), inv_areas[G*G]."""
+    G: int
+    points: np.ndarray
+    inv_areas: np.ndarray
+
+    def inv_area(self, i1: int, i2: int) -> float:
+        return float(self.inv_areas[i1 * self.G + i2])
+
+
+def build_grid(G: int) -> SigmaGrid:
+    pts = np.zeros(max(G, 0) + 1, np.float64)
+    inv = np.zeros(max(G, 0) ** 2, np.float64)
+    check(lib.lmkan_b200_build_grid(int(G), _ptr(pts), _ptr(inv)))
+    return SigmaGrid(int(G), pts, inv)
+
+
+def thresholds(G: int) -> Tuple[np.ndarray, np.ndarray]:
+    """(t64, t32): interval_index(x) == #{k : x >= t[k]} (see include/lmkan_b200.h)."""
+    t64 = np.zeros(max(G - 1, 0), np.float64)
+    t32 = np.zeros(max(G - 1, 0), np.float32)
+    check(lib.lmkan_b200_thresholds(int(G), _ptr(t64), _ptr(t32)))
+    return t64, t32
+
+
+def init_table(n_in: int, n_out: int, G: int, seed: int, init_scale: float = -1.0) -> np.ndarray:
+    """init_layer's table (layer.hpp:69-86), reference layout [G+1][G+1][n_in/2][n_out]."""
+    if n_in <= 0 or n_in % 2 or n_out <= 0 or G < 3:
+        check(lib.lmkan_b200_init_table(int(n_in), int(n_out), int(G), int(seed), float(init_scale), None))
+    P = np.empty((G + 1, G + 1, n_in // 2, n_out), np.float64)
+    check(lib.lmkan_b200_init_table(int(n_in), int(n_out), int(G), int(seed) & (2**64 - 1), float(init_scale),
+                                    _ptr(P)))
+    return P
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Layer:
+    """Prepared device layer (opaque ``lmkan_b200_layer*``): fp32 table in the
+    [out_tile][pair][node][OT] layout, grid constants and locate thresholds."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        n_in, n_out, G, dev, ot = (C.c_int() for _ in range(5))
+        tb = C.c_size_t()
+        check(lib.lmkan_b200_layer_info(self._h, C.byref(n_in), C.byref(n_out), C.byref(G), C.byref(dev),
+                                        C.byref(tb), C.byref(ot)))
+        self.n_in, self.n_out, self.G, self.device = n_in.value, n_out.value, G.value, dev.value
+        self.table_bytes, self.out_tile = tb.value, ot.value
+        self.pairs = self.n_in // 2
+
+    # -- construction -------------------------------------------------------
+    @classmethod
+    def from_host(cls, n_in: int, n_out: int, G: int, P: np.ndarray, gamma: float = 1.0,
+                  device: int = 0) -> "Layer":
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        if P.size != (G + 1) ** 2 * (n_in // 2) * n_out:
+            raise ValueError("layer_create: P has the wrong number of coefficients")
+        h = C.c_void_p()
+        check(lib.lmkan_b200_layer_create(int(n_in), int(n_out), int(G), float(gamma), _ptr(P), int(device),
+                                          C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, n_in: int, n_out: int, G: int, P_dev, gamma: float = 1.0, device: int = 0,
+                    out_range: Optional[Tuple[int, int]] = None) -> "Layer":
+        """P_dev: contiguous float32 CUDA tensor in reference layout."""
+        import torch
+        assert P_dev.dtype == torch.float32 and P_dev.is_cuda and P_dev.is_contiguous()
+        ob, oe = out_range if out_range else (0, n_out)
+        h = C.c_void_p()
+        check(lib.lmkan_b200_layer_create_device_f32_slice(int(n_in), int(n_out), int(G), float(gamma),
+                                                           _ptr(P_dev), int(ob), int(oe), int(device),
+                                                           C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def random(cls, n_in: int, n_out: int, G: int, seed: int = 1234, scale: float = -1.0,
+               gamma: float = 1.0, device: int = 0, out_range: Optional[Tuple[int, int]] = None) -> "Layer":
+        """Table generated on the device (counter-based RNG), N(0, scale^2);
+        scale < 0 selects init_layer's (n_in/2)^-1/2 (layer.hpp:63-65)."""
+        if scale < 0:
+            scale = 1.0 / np.sqrt(max(n_in // 2, 1))
+        ob, oe = out_range if out_range else (0, n_out)
+        h = C.c_void_p()
+        check(lib.lmkan_b200_layer_create_random(int(n_in), int(n_out), int(G), float(gamma), int(seed),
+                                                 float(scale), int(ob), int(oe), int(device), C.byref(h)))
+        return cls(h)
+
+    # -- forward ------------------------------------------------------------
+    def forward_into(self, X, Y, stream=None) -> None:
+        """Device path: X [rows, n_in], Y [rows, n_out] contiguous CUDA tensors
+        (float32 or float64, same dtype); asynchronous on `stream`."""
+        import torch
+        if X.dim() != 2 or X.shape[1] != self.n_in:
+            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
+        assert X.is_cuda and Y.is_cuda and X.is_contiguous() and Y.is_contiguous()
+        assert Y.shape == (X.shape[0], self.n_out) and Y.dtype == X.dtype
+        fn = lib.lmkan_b200_forward_f32 if X.dtype == torch.float32 else lib.lmkan_b200_forward_f64
+        check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream)))
+
+    def forward(self, X, stream=None):
+        """torch CUDA tensor in -> CUDA tensor out; numpy in -> numpy out (host path)."""
+        if isinstance(X, np.ndarray):
+            return self.forward_host(X)
+        import torch
+        Y = torch.empty((X.shape[0], self.n_out), dtype=X.dtype, device=X.device)
+        self.forward_into(X, Y, stream)
+        return Y
+
+    def forward_host(self, X: np.ndarray, Y: Optional[np.ndarray] = None) -> np.ndarray:
+        """Synchronous host path (copies pipelined with the kernel by row chunk)."""
+        if X.ndim != 2 or X.shape[1] != self.n_in:
+            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        if Y is None or Y.shape != (X.shape[0], self.n_out) or Y.dtype != X.dtype:
+            Y = np.empty((X.shape[0], self.n_out), X.dtype)
+        fn = lib.lmkan_b200_forward_host_f32 if X.dtype == np.float32 else lib.lmkan_b200_forward_host_f64
+        check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), 0))
+        return Y
+
+    def forward_host_ptr(self, X_ptr: int, Y_ptr: int, rows: int, dtype=np.float32) -> None:
+        fn = lib.lmkan_b200_forward_host_f32 if dtype == np.float32 else lib.lmkan_b200_forward_host_f64
+        check(fn(self._h, C.c_void_p(X_ptr), C.c_void_p(Y_ptr), int(rows), 0))
+
+    def locate(self, X, stream=None):
+        """Stage 1 only: (i1, i2, w) CUDA tensors, w[..., :] = {w00, w10, w01, w11}."""
+        import torch
+        rows = X.shape[0]
+        i1 = torch.empty((rows, self.pairs), dtype=torch.int32, device=X.device)
+        i2 = torch.empty_like(i1)
+        w = torch.empty((rows, self.pairs, 4), dtype=torch.float32, device=X.device)
+        fn = lib.lmkan_b200_locate_f32 if X.dtype == torch.float32 else lib.lmkan_b200_locate_f64
+        check(fn(self._h, _ptr(X), _ptr(i1), _ptr(i2), _ptr(w), int(rows), _stream_ptr(stream)))
+        return i1, i2, w
+
+    # -- introspection ------------------------------------------------------
+    def set_gamma(self, gamma: float) -> None:
+        check(lib.lmkan_b200_layer_set_gamma(self._h, float(gamma)))
+
+    def read_table(self, pair_begin: int = 0, pair_end: Optional[int] = None) -> np.ndarray:
+        """Device table back in reference layout: [G+1, G+1, pairs, n_out] doubles."""
+        pe = self.pairs if pair_end is None else pair_end
+        out = np.empty((self.G + 1, self.G + 1, pe - pair_begin, self.n_out), np.float64)
+        check(lib.lmkan_b200_layer_read_table(self._h, int(pair_begin), int(pe), _ptr(out)))
+        return out
+
+    def plan(self, rows: int) -> dict:
+        v = [C.c_int() for _ in range(5)]
+        check(lib.lmkan_b200_plan(self._h, int(rows), *[C.byref(x) for x in v]))
+        return dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches"],
+                        [x.value for x in v]))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.lmkan_b200_layer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# Mirror of the reference host interface (layer.hpp:24-134) for Python callers.
+
+@dataclass
+class LmKanLayer:
+    """layer.hpp:24-61. P is the reference table [G+1][G+1][n_in/2][n_out]."""
+    n_in: int
+    n_out: int
+    grid: SigmaGrid
+    P: np.ndarray
+    gamma: float = 0.0
+    device: int = 0
+    _prepared: Optional[Layer] = field(default=None, repr=False, compare=False)
+    _key: Optional[bytes] = field(default=None, repr=False, compare=False)
+
+    def pairs(self) -> int:
+        return self.n_in // 2
+
+    def param_count(self) -> int:
+        return int(self.P.size)
+
+    def prepared(self) -> Layer:
+        """Device handle, rebuilt when P changed since the last call (fingerprint
+        of the full table, so in-place edits of P are never served stale)."""
+        import hashlib
+        P = np.ascontiguousarray(self.P, np.float64)
+        key = hashlib.blake2b(P.view(np.uint8), digest_size=16).digest() + \
+            np.array([self.n_in, self.n_out, self.grid.G], np.int64).tobytes()
+        if self._prepared is None or key != self._key:
+            if self._prepared is not None:
+                self._prepared.close()
+            self._prepared = Layer.from_host(self.n_in, self.n_out, self.grid.G, P, self.gamma, self.device)
+            self._key = key
+        self._prepared.set_gamma(self.gamma)
+        return self._prepared
+
+
+def init_layer(n_in: int, n_out: int, G: int, seed: int, init_scale: float = -1.0) -> LmKanLayer:
+    """layer.hpp:69-86: same validation, same table, gamma = 0."""
+    P = init_table(n_in, n_out, G, seed, init_scale)
+    return LmKanLayer(n_in, n_out, build_grid(G), P, 0.0)
+
+
+def lmkan_forward(layer: LmKanLayer, X: np.ndarray, Y: Optional[np.ndarray] = None,
+                  workers: int = 0) -> np.ndarray:
+    """layer.hpp:108-134 on the B200: X [rows, n_in] float64 host array; returns
+    Y [rows, n_out] (reused when the shape matches, else reallocated, like
+    layer.hpp:111-112). `workers` is accepted and ignored."""
+    X = np.asarray(X)
+    if X.ndim != 2 or X.shape[1] != layer.n_in:
+        width = X.shape[1] if X.ndim == 2 else X.shape[-1]
+        raise ValueError(f"lmkan_forward: expected width {layer.n_in}, got {width}")
+    X = np.ascontiguousarray(X, np.float64)
+    if Y is None or Y.shape != (X.shape[0], layer.n_out) or Y.dtype != np.float64 or not Y.flags.c_contiguous:
+        Y = np.zeros((X.shape[0], layer.n_out), np.float64)
+    if X.shape[0] == 0:
+        return Y
+    return layer.prepared().forward_host(X, Y)

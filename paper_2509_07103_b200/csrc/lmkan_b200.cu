@@ -1,0 +1,531 @@
+// C-ABI implementation of include/lmkan_b200.h (host side of the B200 path).
+//
+// Replaces, per DESIGN.md "Boundary":
+//   lmkan::build_grid            grid.hpp:44-68     -> lmkan_b200_build_grid
+//   lmkan::interval_index        grid.hpp:72-75     -> lmkan_b200_thresholds (+ device search)
+//   lmkan::LmKanLayer + P        layer.hpp:24-61    -> lmkan_b200_layer (prepared device table)
+//   lmkan::lmkan_forward         layer.hpp:108-134  -> lmkan_b200_forward_{f32,f64,host_f32,host_f64}
+//   lmkan::detail::row_preambles layer.hpp:96-101   -> lmkan_b200_locate_{f32,f64}
+// There is no CPU compute fallback: without an sm_100a device every compute
+// entry point fails with LMKAN_B200_ENOSYS / ECUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lmkan_b200.h"
+#include "grid_host.hpp"
+#include "host_rng.hpp"
+#include "kernels.cuh"
+
+using namespace lmkan_b200;
+
+struct lmkan_b200_layer {
+    int device = 0;
+    int n_in = 0, n_out = 0, G = 0, pairs = 0, nodes = 0;
+    int n_out_total = 0, out_begin = 0;
+    double gamma = 0.0;
+    int OT = 64, n_ot = 0;
+    float* table = nullptr;
+    size_t table_bytes = 0;
+    double* d_inv = nullptr;
+    GridConst gc{};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(LMKAN_B200_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    if (e == cudaErrorNoKernelImageForDevice || e == cudaErrorInvalidDeviceFunction ||
+        e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return fail(LMKAN_B200_ENOSYS, std::string(what) + ": " + cudaGetErrorString(e));
+    return fail(LMKAN_B200_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int require_sm100(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(LMKAN_B200_ENOSYS, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(LMKAN_B200_EINVAL, "device ordinal out of range");
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0)
+        return fail(LMKAN_B200_ENOSYS, "kernels are built for sm_100a (B200); device is sm_" +
+                                           std::to_string(major) + std::to_string(minor));
+    return LMKAN_B200_OK;
+}
+
+int max_smem_optin(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    return v > 0 ? v : 232448;
+}
+
+// ---------------------------------------------------------------- planning
+struct Plan {
+    int OT, RT, nbuf, R;
+    uint32_t smem;
+    int64_t row_tiles;
+};
+
+constexpr int kRTChoices[] = {16, 8, 4};
+
+int rows_per_cta(int OT, int RT) { return kWarps * (32 / (OT / 4)) * RT; }
+
+// Output tile width for a layer: the widest of {128, 64, 32, 16} (not wider
+// than the padded layer) whose sheet can be double-buffered next to the
+// record rings at the largest row tile.
+int choose_out_tile(int n_out, int G, int smem_cap) {
+    if (const char* e = std::getenv("LMKAN_B200_OT")) {
+        const int v = std::atoi(e);
+        if (v == 16 || v == 32 || v == 64 || v == 128) return v;
+    }
+    const int nodes = (G + 1) * (G + 1);
+    const int cands[] = {64, 32, 16};
+    for (int OT : cands) {
+        if (OT > 16 && OT / 2 >= n_out) continue;  // do not pad small layers 2x
+        for (int RT : kRTChoices) {
+            const FusedSmem s = fused_smem_layout(nodes, OT, rows_per_cta(OT, RT), 2);
+            if (static_cast<int>(s.total) <= smem_cap) return OT;
+        }
+    }
+    return 16;
+}
+
+bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
+    int force_rt = 0, force_nbuf = 0;
+    if (const char* e = std::getenv("LMKAN_B200_RT")) force_rt = std::atoi(e);
+    if (const char* e = std::getenv("LMKAN_B200_NBUF")) force_nbuf = std::atoi(e);
+    const int num_sms = 148;
+    bool found = false;
+    for (int RT : kRTChoices) {
+        if (force_rt && RT != force_rt) continue;
+        const int R = rows_per_cta(L->OT, RT);
+        const int64_t tiles = (rows + R - 1) / R;
+        // keep >= ~1 wave of CTAs when the batch allows it
+        if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < num_sms) continue;
+        for (int nbuf = 4; nbuf >= 1; --nbuf) {
+            if (force_nbuf && nbuf != force_nbuf) continue;
+            if (nbuf > L->pairs && nbuf > 1) continue;
+            const FusedSmem s = fused_smem_layout(L->nodes, L->OT, R, nbuf);
+            if (static_cast<int>(s.total) > smem_cap) continue;
+            out = Plan{L->OT, RT, nbuf, R, s.total, tiles};
+            found = true;
+            break;
+        }
+        if (found) break;
+    }
+    return found;
+}
+
+template <int OT, int RT, typename XT>
+cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                           cudaStream_t st) {
+    auto kern = fwd_fused_kernel<OT, RT, XT>;
+    static thread_local int configured_smem[64] = {0};
+    const int dev = L->device;
+    if (configured_smem[dev & 63] < static_cast<int>(pl.smem)) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return e;
+        configured_smem[dev & 63] = 232448;
+    }
+    dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
+    kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf,
+                                           static_cast<float>(L->gamma), L->gc);
+    return cudaGetLastError();
+}
+
+template <int OT, typename XT>
+cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                            cudaStream_t st) {
+    switch (pl.RT) {
+        case 16: return launch_fused_t<OT, 16, XT>(L, pl, X, Y, rows, st);
+        case 8: return launch_fused_t<OT, 8, XT>(L, pl, X, Y, rows, st);
+        default: return launch_fused_t<OT, 4, XT>(L, pl, X, Y, rows, st);
+    }
+}
+
+template <typename XT>
+int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
+    if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
+    if (rows == 0) return LMKAN_B200_OK;
+    if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
+    if (reinterpret_cast<uintptr_t>(Y) % 16 != 0)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: Y must be 16-byte aligned");
+    DeviceGuard g(L->device);
+    Plan pl;
+    if (!make_plan(L, rows, max_smem_optin(L->device), pl))
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory (G too large)");
+    if (pl.row_tiles > 0x7fffffff) return fail(LMKAN_B200_EINVAL, "lmkan_forward: batch too large");
+    cudaError_t e;
+    switch (L->OT) {
+        case 128: e = launch_fused_rt<128, XT>(L, pl, X, Y, rows, st); break;
+        case 64: e = launch_fused_rt<64, XT>(L, pl, X, Y, rows, st); break;
+        case 32: e = launch_fused_rt<32, XT>(L, pl, X, Y, rows, st); break;
+        default: e = launch_fused_rt<16, XT>(L, pl, X, Y, rows, st); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: fused kernel launch");
+    return LMKAN_B200_OK;
+}
+
+template <typename XT>
+int locate_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t* i2, float* w, int64_t rows,
+                  cudaStream_t st) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "locate: null layer");
+    if (rows <= 0) return rows == 0 ? LMKAN_B200_OK : fail(LMKAN_B200_EINVAL, "locate: negative rows");
+    if (reinterpret_cast<uintptr_t>(w) % 16 != 0) return fail(LMKAN_B200_EINVAL, "locate: w must be 16-byte aligned");
+    DeviceGuard g(L->device);
+    const int64_t total = rows * L->pairs;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+    locate_kernel<XT><<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, rows, L->n_in, L->gc, i1, i2,
+                                                                     reinterpret_cast<float4*>(w));
+    CK(cudaGetLastError());
+    return LMKAN_B200_OK;
+}
+
+int validate_shape(int n_in, int n_out, int G) {
+    if (n_in <= 0 || n_in % 2 != 0)
+        return fail(LMKAN_B200_EINVAL, "init_layer: n_in must be a positive even number");
+    if (n_out <= 0) return fail(LMKAN_B200_EINVAL, "init_layer: n_out must be positive");
+    if (G < 3) return fail(LMKAN_B200_EINVAL, "build_grid: G must be >= 3 (ghost rule needs two interior points)");
+    if (G > kMaxThr) return fail(LMKAN_B200_EINVAL, "build_grid: G > 64 is not supported by the B200 kernels");
+    return LMKAN_B200_OK;
+}
+
+// Allocates the handle, grid constants and the (uninitialised) device table.
+int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,
+                lmkan_b200_layer** out) {
+    if (!out) return fail(LMKAN_B200_EINVAL, "layer_create: null out pointer");
+    *out = nullptr;
+    if (int rc = validate_shape(n_in, n_out_total, G)) return rc;
+    if (out_begin < 0 || n_out_local <= 0 || out_begin + n_out_local > n_out_total)
+        return fail(LMKAN_B200_EINVAL, "layer_create: bad output slice");
+    if (int rc = require_sm100(device)) return rc;
+    DeviceGuard g(device);
+    auto* L = new lmkan_b200_layer();
+    L->device = device;
+    L->n_in = n_in;
+    L->n_out = n_out_local;
+    L->n_out_total = n_out_total;
+    L->out_begin = out_begin;
+    L->G = G;
+    L->pairs = n_in / 2;
+    L->nodes = (G + 1) * (G + 1);
+    L->gamma = gamma;
+    L->OT = choose_out_tile(n_out_local, G, max_smem_optin(device));
+    L->n_ot = (n_out_local + L->OT - 1) / L->OT;
+    std::vector<double> pts, inv, t64;
+    std::vector<float> t32;
+    host::build_grid(G, pts, inv);
+    host::thresholds(G, t64, t32);
+    GridConst& gc = L->gc;
+    gc.G = G;
+    gc.L = 1;
+    while (gc.L < G) gc.L <<= 1;
+    const float fnan = std::numeric_limits<float>::quiet_NaN();
+    const double dnan = std::numeric_limits<double>::quiet_NaN();
+    for (int k = 0; k < kMaxThr; ++k) {
+        gc.t32[k] = k < G - 1 ? t32[k] : fnan;
+        gc.t64[k] = k < G - 1 ? t64[k] : dnan;
+    }
+    for (int k = 0; k <= kMaxThr; ++k) gc.points[k] = k <= G ? pts[k] : 0.0;
+    L->table_bytes = static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->OT * sizeof(float);
+    cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(L->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&L->table, L->table_bytes);
+    if (e != cudaSuccess) {
+        cudaFree(L->d_inv);
+        delete L;
+        return cuda_fail(e, "layer_create: device allocation");
+    }
+    gc.inv_areas = L->d_inv;
+    *out = L;
+    return LMKAN_B200_OK;
+}
+
+unsigned fill_blocks(size_t total) {
+    return static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 64));
+}
+
+template <typename T>
+int relayout_from_device(lmkan_b200_layer* L, const T* P_dev) {
+    const size_t total = L->table_bytes / sizeof(float);
+    relayout_kernel<T><<<fill_blocks(total), 256>>>(P_dev, L->table, L->pairs, L->nodes, L->n_out_total,
+                                                    L->out_begin, L->n_out, L->OT, L->n_ot);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    return LMKAN_B200_OK;
+}
+
+// Host-path streams (per device, per host thread) for the chunked H2D/compute/D2H pipeline.
+struct HostStreams {
+    cudaStream_t s[2] = {nullptr, nullptr};
+};
+
+template <typename XT>
+int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
+    if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
+    if (rows == 0) return LMKAN_B200_OK;
+    if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
+    DeviceGuard g(L->device);
+    static thread_local HostStreams hs[64];
+    HostStreams& H = hs[L->device & 63];
+    for (auto& s : H.s)
+        if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // Chunk so the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernel.
+    Plan pl;
+    if (!make_plan(L, rows, max_smem_optin(L->device), pl))
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
+    const int64_t min_chunk = static_cast<int64_t>(pl.R) * 148 / std::max(1, L->n_ot);
+    int64_t chunk = std::max<int64_t>({(rows + 7) / 8, min_chunk, 1});
+    chunk = std::min(chunk, rows);
+    const size_t xb = static_cast<size_t>(chunk) * L->n_in * sizeof(XT);
+    const size_t yb = static_cast<size_t>(chunk) * L->n_out * sizeof(XT);
+    XT* dX[2] = {nullptr, nullptr};
+    XT* dY[2] = {nullptr, nullptr};
+    int rc = LMKAN_B200_OK;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dX[i]), xb, H.s[i]));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dY[i]), yb, H.s[i]));
+    }
+    int c = 0;
+    for (int64_t r0 = 0; r0 < rows && rc == LMKAN_B200_OK; r0 += chunk, ++c) {
+        const int i = c & 1;
+        const int64_t n = std::min(chunk, rows - r0);
+        cudaError_t e = cudaMemcpyAsync(dX[i], X + r0 * L->n_in, static_cast<size_t>(n) * L->n_in * sizeof(XT),
+                                        cudaMemcpyHostToDevice, H.s[i]);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "lmkan_forward: H2D"); break; }
+        rc = forward_device<XT>(L, dX[i], dY[i], n, H.s[i]);
+        if (rc) break;
+        e = cudaMemcpyAsync(Y + r0 * L->n_out, dY[i], static_cast<size_t>(n) * L->n_out * sizeof(XT),
+                            cudaMemcpyDeviceToHost, H.s[i]);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "lmkan_forward: D2H"); break; }
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeAsync(dX[i], H.s[i]);
+        cudaFreeAsync(dY[i], H.s[i]);
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaError_t e = cudaStreamSynchronize(H.s[i]);
+        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = cuda_fail(e, "lmkan_forward: stream sync");
+    }
+    return rc;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* lmkan_b200_last_error(void) { return g_err.c_str(); }
+
+const char* lmkan_b200_version(void) { return "lmkan_b200 0.1 (sm_100a, fused locate+gather, bulk-copy sheets)"; }
+
+int lmkan_b200_build_grid(int G, double* points, double* inv_areas) {
+    std::vector<double> p, inv;
+    if (!host::build_grid(G, p, inv))
+        return fail(LMKAN_B200_EINVAL, "build_grid: G must be >= 3 (ghost rule needs two interior points)");
+    if (points) std::memcpy(points, p.data(), sizeof(double) * p.size());
+    if (inv_areas) std::memcpy(inv_areas, inv.data(), sizeof(double) * inv.size());
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_thresholds(int G, double* t64, float* t32) {
+    std::vector<double> a;
+    std::vector<float> b;
+    if (!host::thresholds(G, a, b))
+        return fail(LMKAN_B200_EINVAL, "build_grid: G must be >= 3 (ghost rule needs two interior points)");
+    if (t64) std::memcpy(t64, a.data(), sizeof(double) * a.size());
+    if (t32) std::memcpy(t32, b.data(), sizeof(float) * b.size());
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_init_table(int n_in, int n_out, int G, uint64_t seed, double init_scale, double* P_out) {
+    if (n_in <= 0 || n_in % 2 != 0)
+        return fail(LMKAN_B200_EINVAL, "init_layer: n_in must be a positive even number");
+    if (n_out <= 0) return fail(LMKAN_B200_EINVAL, "init_layer: n_out must be positive");
+    if (G < 3) return fail(LMKAN_B200_EINVAL, "build_grid: G must be >= 3 (ghost rule needs two interior points)");
+    if (!P_out) return fail(LMKAN_B200_EINVAL, "init_layer: null output");
+    if (init_scale < 0.0) init_scale = 1.0 / std::sqrt(static_cast<double>(n_in / 2));
+    const size_t count = static_cast<size_t>(G + 1) * (G + 1) * (n_in / 2) * n_out;
+    host::NamedStream rs(seed, "lmkan.layer.init");
+    for (size_t i = 0; i < count; ++i) P_out[i] = init_scale * rs.normal();
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_layer_create(int n_in, int n_out, int G, double gamma, const double* P_host, int device,
+                            lmkan_b200_layer** out) {
+    if (!P_host) return fail(LMKAN_B200_EINVAL, "layer_create: null P");
+    if (int rc = alloc_layer(n_in, n_out, n_out, 0, G, gamma, device, out)) return rc;
+    lmkan_b200_layer* L = *out;
+    DeviceGuard g(device);
+    const size_t count = static_cast<size_t>(L->nodes) * L->pairs * n_out;
+    double* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, count * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(tmp, P_host, count * sizeof(double), cudaMemcpyHostToDevice);
+    int rc = e == cudaSuccess ? relayout_from_device<double>(L, tmp) : cuda_fail(e, "layer_create: upload P");
+    cudaFree(tmp);
+    if (rc) {
+        lmkan_b200_layer_destroy(L);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int lmkan_b200_layer_create_device_f32_slice(int n_in, int n_out, int G, double gamma, const float* P_dev,
+                                             int out_begin, int out_end, int device, lmkan_b200_layer** out) {
+    if (!P_dev) return fail(LMKAN_B200_EINVAL, "layer_create: null P");
+    if (int rc = alloc_layer(n_in, out_end - out_begin, n_out, out_begin, G, gamma, device, out)) return rc;
+    DeviceGuard g(device);
+    int rc = relayout_from_device<float>(*out, P_dev);
+    if (rc) {
+        lmkan_b200_layer_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int lmkan_b200_layer_create_device_f32(int n_in, int n_out, int G, double gamma, const float* P_dev, int device,
+                                       lmkan_b200_layer** out) {
+    return lmkan_b200_layer_create_device_f32_slice(n_in, n_out, G, gamma, P_dev, 0, n_out, device, out);
+}
+
+int lmkan_b200_layer_create_random(int n_in, int n_out, int G, double gamma, uint64_t seed, double scale,
+                                   int out_begin, int out_end, int device, lmkan_b200_layer** out) {
+    if (int rc = alloc_layer(n_in, out_end - out_begin, n_out, out_begin, G, gamma, device, out)) return rc;
+    lmkan_b200_layer* L = *out;
+    DeviceGuard g(device);
+    const size_t total = L->table_bytes / sizeof(float);
+    fill_random_kernel<<<fill_blocks(total), 256>>>(L->table, L->pairs, L->nodes, L->n_out_total, L->out_begin,
+                                                    L->n_out, L->OT, L->n_ot, seed, static_cast<float>(scale));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        lmkan_b200_layer_destroy(L);
+        *out = nullptr;
+        return cuda_fail(e, "layer_create_random: fill");
+    }
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_layer_read_table(const lmkan_b200_layer* L, int pair_begin, int pair_end, double* dst) {
+    if (!L || !dst) return fail(LMKAN_B200_EINVAL, "read_table: null argument");
+    if (pair_begin < 0 || pair_end > L->pairs || pair_begin >= pair_end)
+        return fail(LMKAN_B200_EINVAL, "read_table: bad pair range");
+    DeviceGuard g(L->device);
+    const size_t count = static_cast<size_t>(L->nodes) * (pair_end - pair_begin) * L->n_out;
+    double* tmp = nullptr;
+    CK(cudaMalloc(&tmp, count * sizeof(double)));
+    export_kernel<<<fill_blocks(count), 256>>>(L->table, tmp, L->pairs, L->nodes, L->n_out, L->OT, pair_begin,
+                                               pair_end);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "read_table");
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_layer_set_gamma(lmkan_b200_layer* L, double gamma) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "set_gamma: null layer");
+    L->gamma = gamma;
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_layer_info(const lmkan_b200_layer* L, int* n_in, int* n_out, int* G, int* device,
+                          size_t* table_bytes, int* out_tile) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "layer_info: null layer");
+    if (n_in) *n_in = L->n_in;
+    if (n_out) *n_out = L->n_out;
+    if (G) *G = L->G;
+    if (device) *device = L->device;
+    if (table_bytes) *table_bytes = L->table_bytes;
+    if (out_tile) *out_tile = L->OT;
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_layer_destroy(lmkan_b200_layer* L) {
+    if (!L) return LMKAN_B200_OK;
+    {
+        DeviceGuard g(L->device);
+        cudaFree(L->table);
+        cudaFree(L->d_inv);
+    }
+    delete L;
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_forward_f32(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, void* stream) {
+    return forward_device<float>(L, X, Y, rows, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_forward_f64(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, void* stream) {
+    return forward_device<double>(L, X, Y, rows, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_forward_host_f64(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows,
+                                size_t /*workers*/) {
+    return forward_host<double>(L, X, Y, rows);
+}
+int lmkan_b200_forward_host_f32(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows,
+                                size_t /*workers*/) {
+    return forward_host<float>(L, X, Y, rows);
+}
+int lmkan_b200_locate_f32(const lmkan_b200_layer* L, const float* X, int32_t* i1, int32_t* i2, float* w,
+                          int64_t rows, void* stream) {
+    return locate_device<float>(L, X, i1, i2, w, rows, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i1, int32_t* i2, float* w,
+                          int64_t rows, void* stream) {
+    return locate_device<double>(L, X, i1, i2, w, rows, static_cast<cudaStream_t>(stream));
+}
+
+int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
+                    int* rows_per_cta_out, int* launches) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
+    Plan pl;
+    if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits");
+    if (out_tile) *out_tile = pl.OT;
+    if (rows_per_thread) *rows_per_thread = pl.RT;
+    if (nbuf) *nbuf = pl.nbuf;
+    if (rows_per_cta_out) *rows_per_cta_out = pl.R;
+    if (launches) *launches = 1;
+    return LMKAN_B200_OK;
+}
+
+}  // extern "C"

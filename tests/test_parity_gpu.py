@@ -1,0 +1,230 @@
+"""GPU parity tests: the sm_100a path through the C-ABI vs the oracle.
+
+Oracle = the reference's own lmkan_forward / row_preambles compiled from
+/root/reference (oracle/_ref) when present, else the C restatement (oracle/).
+Same inputs for both: fp32 X and fp32 P, widened exactly to double for the
+oracle. Bars:
+  * cell indices (i1, i2) bit-exact; weights == fp32(reference fp64 weight);
+  * outputs |y - y_ref| <= 1e-5 * max(1, |y_ref|), the reference's own
+    normalization (test_layer.cpp:96-97).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2509_07103_b200 as p
+    return p
+
+
+def _mixed(y, ref):
+    import pyoracle
+    return pyoracle.mixed_err(y, ref)
+
+
+def _inputs(torch, n_in, n_out, G, rows, seed, xscale=1.0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    P = torch.randn((G + 1, G + 1, n_in // 2, n_out), generator=g, dtype=torch.float32) / np.sqrt(n_in // 2)
+    X = torch.randn((rows, n_in), generator=g, dtype=torch.float32) * xscale
+    return P.numpy(), X.numpy()
+
+
+def _special_rows(n_in, G, pkg):
+    """Rows built from the reference's edge cases: thresholds +-1 ulp, +-0,
+    tiny negatives (exp(-|x|) rounds to 1), huge, +-inf, NaN."""
+    t64, t32 = pkg.thresholds(G)
+    vals = [0.0, -0.0, 1e-45, -1e-45, -1e-30, 1e-30, -5e-17, 5e-17, 3e38, -3e38, np.inf, -np.inf, np.nan,
+            100.0, -100.0]
+    for t in t32:
+        vals += [np.nextafter(t, -np.inf, dtype=np.float32), t, np.nextafter(t, np.inf, dtype=np.float32)]
+    vals = np.array(vals, np.float32)
+    reps = int(np.ceil(vals.size * 2 / n_in)) + 1
+    rng = np.random.default_rng(G)
+    out = np.concatenate([rng.permutation(vals) for _ in range(reps * n_in // vals.size + 2)])
+    return out[: reps * n_in].reshape(reps, n_in)
+
+
+SHAPES = [  # (n_in, n_out, G, rows) — BASELINE.json configs, row subsets where the oracle is slow
+    (64, 64, 8, 1024),      # cfg1
+    (1024, 1024, 16, 300),  # cfg2 (row subset)
+    (12, 128, 28, 4096),    # cfg3 layer 1
+    (128, 128, 28, 2048),   # cfg3 layer 2
+    (128, 1, 28, 4096),     # cfg3 head
+    (144, 16, 16, 4096),    # cfg4 stage 1
+    (288, 32, 16, 2048),    # cfg4 stage 2
+    (576, 64, 16, 1024),    # cfg4 stage 3
+]
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows", SHAPES)
+def test_locate_bit_exact(torch, pkg, oracle, n_in, n_out, G, rows):
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in + G)
+    X = np.concatenate([X, _special_rows(n_in, G, pkg)])
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    i1, i2, w = layer.locate(torch.from_numpy(X).cuda())
+    r1, r2, rw = oracle.locate(G, X.astype(np.float64))
+    assert np.array_equal(i1.cpu().numpy(), r1)
+    assert np.array_equal(i2.cpu().numpy(), r2)
+    np.testing.assert_array_equal(w.cpu().numpy(), rw.astype(np.float32))
+
+
+@pytest.mark.parametrize("G", [3, 4, 5, 8, 12, 13, 16, 28, 32, 40, 64])
+def test_locate_f64_near_thresholds(torch, pkg, oracle, G):
+    """Double inputs that are not fp32-representable, packed around every
+    threshold: the f64 path compares against the fp64 thresholds."""
+    t64, _ = pkg.thresholds(G)
+    xs = []
+    for t in t64:
+        x = t
+        for _ in range(40):
+            x = np.nextafter(x, -np.inf)
+        for _ in range(80):
+            xs.append(x)
+            x = np.nextafter(x, np.inf)
+    xs += [0.0, -0.0, -1e-300, 1e-300, -2.0 ** -54, -2.0 ** -53, np.inf, -np.inf, np.nan, 1e308, -1e308]
+    xs = np.array(xs)
+    if xs.size % 2:
+        xs = np.append(xs, 0.25)
+    X = xs.reshape(-1, 2)
+    layer = pkg.Layer.random(2, 4, G, seed=1)
+    i1, i2, w = layer.locate(torch.from_numpy(X).cuda())
+    r1, r2, rw = oracle.locate(G, X)
+    assert np.array_equal(i1.cpu().numpy(), r1)
+    assert np.array_equal(i2.cpu().numpy(), r2)
+    np.testing.assert_array_equal(w.cpu().numpy(), rw.astype(np.float32))
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows", SHAPES)
+def test_forward_parity(torch, pkg, oracle, n_in, n_out, G, rows):
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=3 * n_in + G)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 1.0)
+    err = _mixed(Y, ref)
+    assert err.max() <= TOL, f"max mixed err {err.max():.3e}"
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows,gamma", [
+    (2, 1, 5, 64, 1.0), (6, 5, 3, 64, 0.8), (6, 5, 12, 64, 0.8), (8, 3, 4, 33, 0.6), (8, 6, 12, 33, 0.9),
+    (4, 3, 4, 16, 0.0), (10, 7, 64, 130, 1.0), (30, 100, 9, 777, 1.3), (16, 20, 6, 1, 1.0),
+    (64, 200, 8, 5000, 1.0), (256, 48, 20, 3001, 0.5),
+])
+def test_forward_small_and_ragged(torch, pkg, oracle, n_in, n_out, G, rows, gamma):
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in * 7 + n_out + G, xscale=1.5)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), gamma)
+    Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), gamma)
+    assert _mixed(Y, ref).max() <= TOL
+
+
+def test_forward_nonfinite_inputs(torch, pkg, oracle):
+    """+-inf / NaN inputs propagate like the reference: same NaN and +-inf
+    positions, finite outputs within tolerance. (|x| is kept where the fp64
+    weights stay inside fp32 range; beyond that fp32 outputs cannot represent
+    the reference's finite huge values.)"""
+    n_in, n_out, G = 32, 16, 8
+    P, _ = _inputs(torch, n_in, n_out, G, 1, seed=5)
+    X = _special_rows(n_in, G, pkg)
+    X[np.isfinite(X) & (np.abs(X) > 1e4)] = 1e4
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 1.0)
+    assert np.array_equal(np.isnan(Y), np.isnan(ref))
+    assert np.array_equal(np.isposinf(Y), np.isposinf(ref))
+    assert np.array_equal(np.isneginf(Y), np.isneginf(ref))
+    fin = np.isfinite(ref)
+    assert _mixed(Y[fin], ref[fin]).max() <= TOL
+
+
+def test_forward_deterministic_and_shard_invariant(torch, pkg):
+    n_in, n_out, G, rows = 256, 192, 16, 5000
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=11)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    Xd = torch.from_numpy(X).cuda()
+    Y1 = layer.forward(Xd)
+    Y2 = layer.forward(Xd)
+    assert torch.equal(Y1, Y2)
+    # batch sharding (configs 1-4): any row split gives bitwise-identical rows
+    parts = [layer.forward(Xd[a:b].contiguous()) for a, b in [(0, 1000), (1000, 1001), (1001, rows)]]
+    assert torch.equal(torch.cat(parts), Y1)
+    # output sharding (config 5): output-sliced layers reproduce columns bitwise
+    Pd = torch.from_numpy(P).cuda()
+    for ob, oe in [(0, 64), (64, 130), (130, 192)]:
+        sl = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0, out_range=(ob, oe))
+        assert torch.equal(sl.forward(Xd), Y1[:, ob:oe])
+
+
+def test_table_roundtrip(torch, pkg):
+    n_in, n_out, G = 12, 40, 5
+    P, _ = _inputs(torch, n_in, n_out, G, 1, seed=2)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    np.testing.assert_array_equal(layer.read_table(), P.astype(np.float64))
+    np.testing.assert_array_equal(layer.read_table(2, 5), P[:, :, 2:5].astype(np.float64))
+    sl = pkg.Layer.from_device(n_in, n_out, G, torch.from_numpy(P).cuda(), 1.0, out_range=(7, 33))
+    np.testing.assert_array_equal(sl.read_table(), P[..., 7:33].astype(np.float64))
+
+
+def test_random_table_layer_matches_oracle(torch, pkg, oracle):
+    n_in, n_out, G, rows = 64, 96, 8, 700
+    layer = pkg.Layer.random(n_in, n_out, G, seed=99)
+    P = layer.read_table()
+    assert abs(P.std() * np.sqrt(n_in // 2) - 1.0) < 0.05
+    _, X = _inputs(torch, n_in, n_out, G, rows, seed=4)
+    Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = oracle.forward(G, P, X.astype(np.float64), 1.0)
+    assert _mixed(Y, ref).max() <= TOL
+
+
+def test_host_paths(torch, pkg, oracle):
+    """Drop-in host entry points (lmkan_forward semantics on host memory)."""
+    n_in, n_out, G, rows = 48, 40, 8, 3000
+    rng = np.random.default_rng(1)
+    P = rng.normal(size=(G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)  # full fp64 table
+    X = rng.normal(size=(rows, n_in))  # fp64, not fp32-representable
+    lay = pkg.init_layer(n_in, n_out, G, seed=5)
+    lay.P = P
+    lay.gamma = 0.7
+    Y = pkg.lmkan_forward(lay, X)
+    ref = oracle.forward(G, P, X, 0.7)
+    assert _mixed(Y, ref).max() <= TOL
+    # in-place table edit is never served stale
+    lay.P[0, 0, 0, 0] += 5.0
+    Y2 = pkg.lmkan_forward(lay, X)
+    ref2 = oracle.forward(G, lay.P, X, 0.7)
+    assert _mixed(Y2, ref2).max() <= TOL
+    # fp32 host path
+    layer = lay.prepared()
+    Xf = X.astype(np.float32)
+    Yf = layer.forward_host(Xf)
+    reff = oracle.forward(G, P.astype(np.float32).astype(np.float64) + 0.0, Xf.astype(np.float64), 0.7)
+    reff = oracle.forward(G, layer.read_table(), Xf.astype(np.float64), 0.7)
+    assert _mixed(Yf, reff).max() <= TOL
+    with pytest.raises(ValueError, match="expected width 48, got 50"):
+        pkg.lmkan_forward(lay, np.zeros((3, 50)))
+
+
+def test_init_layer_forward_zero_gamma(torch, pkg):
+    lay = pkg.init_layer(4, 3, 4, 123)
+    assert lay.gamma == 0.0
+    Y = pkg.lmkan_forward(lay, np.random.default_rng(0).normal(size=(16, 4)))
+    assert (Y == 0).all()
+
+
+def test_f64_device_path(torch, pkg, oracle):
+    n_in, n_out, G, rows = 40, 24, 13, 999
+    layer = pkg.Layer.random(n_in, n_out, G, seed=3)
+    X = np.random.default_rng(2).normal(size=(rows, n_in)) * 2
+    Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = oracle.forward(G, layer.read_table(), X, 1.0)
+    assert _mixed(Y, ref).max() <= TOL
