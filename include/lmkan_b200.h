@@ -132,10 +132,13 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, in
                           int32_t* i2, float* w, int64_t rows, void* stream);
 
 /* Tuning / introspection: kernel variant chosen for `rows` (OT = output tile,
- * RT = rows per thread, NBUF = sheet buffers, rows_per_cta), and the number of
- * kernel launches one forward issues. */
+ * RT = rows per thread, NBUF = sheet buffers, rows_per_cta), the number of
+ * kernel launches one forward issues and the mode (0 = fused locate+gather,
+ * 1 = staged: cell-record kernel + gather kernel, 2 = global-sheet fallback).
+ * Environment overrides for experiments: LMKAN_B200_MODE=fused|staged|global,
+ * LMKAN_B200_RT, LMKAN_B200_NBUF, LMKAN_B200_OT (at layer creation). */
 int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
-                    int* nbuf, int* rows_per_cta, int* launches);
+                    int* nbuf, int* rows_per_cta, int* launches, int* mode);
 
 #ifdef __cplusplus
 }

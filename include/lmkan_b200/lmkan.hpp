@@ -1,0 +1,254 @@
+// lmkan_b200/lmkan.hpp — C++ host API of the B200 lmKAN layer forward.
+//
+// Restates the reference's layer interface (paths relative to
+// /root/reference/proj/include/lmkan/) on top of the C-ABI in lmkan_b200.h:
+//   Matrix, require_width          matrix.hpp:11-44
+//   SigmaGrid, build_grid           grid.hpp:33-68
+//   interval_index                  grid.hpp:72-75 (threshold form, bit-exact)
+//   LmKanLayer                      layer.hpp:24-61 (same fields and P layout)
+//   default_init_scale, init_layer  layer.hpp:63-86 (bit-identical table)
+//   lmkan_forward                   layer.hpp:108-134 (same signature)
+// Existing callers switch with `namespace lmkan = lmkan_b200;` (see
+// INTEGRATION.md). Errors: std::invalid_argument where the reference throws it
+// (same messages), std::runtime_error for CUDA failures. There is no CPU
+// compute path: lmkan_forward runs on the layer's GPU (LmKanLayer::device).
+//
+// The layer keeps a prepared device table (fp32, [out_tile][pair][node][OT])
+// next to the host P. It is rebuilt whenever P or the shape changed since the
+// last forward (a 64-bit fingerprint of the whole table is checked per call);
+// call freeze() to promise P will not change and skip the fingerprint.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../lmkan_b200.h"
+
+namespace lmkan_b200 {
+
+namespace detail {
+inline void throw_status(int rc, const char* where) {
+    if (rc == LMKAN_B200_OK) return;
+    const std::string msg = lmkan_b200_last_error();
+    if (rc == LMKAN_B200_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(std::string(where) + ": " + msg);
+}
+}  // namespace detail
+
+// Dense row-major matrix of doubles, rows = batch (matrix.hpp:11-38).
+class Matrix {
+public:
+    Matrix() = default;
+    Matrix(std::size_t rows, std::size_t cols, double fill = 0.0)
+        : rows_(rows), cols_(cols), data_(rows * cols, fill) {}
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    std::size_t size() const { return data_.size(); }
+    double& operator()(std::size_t r, std::size_t c) { return data_[r * cols_ + c]; }
+    double operator()(std::size_t r, std::size_t c) const { return data_[r * cols_ + c]; }
+    double* row(std::size_t r) { return data_.data() + r * cols_; }
+    const double* row(std::size_t r) const { return data_.data() + r * cols_; }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    void fill(double v) { std::fill(data_.begin(), data_.end(), v); }
+    bool same_shape(const Matrix& o) const { return rows_ == o.rows_ && cols_ == o.cols_; }
+
+private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<double> data_;
+};
+
+// matrix.hpp:40-44 — same exception type and message.
+inline void require_width(const Matrix& m, std::size_t cols, const char* what) {
+    if (m.cols() != cols)
+        throw std::invalid_argument(std::string(what) + ": expected width " + std::to_string(cols) + ", got " +
+                                    std::to_string(m.cols()));
+}
+
+// grid.hpp:33-39
+struct SigmaGrid {
+    int G = 0;
+    std::vector<double> points;     // G+1, ghost points at both ends
+    std::vector<double> inv_areas;  // G*G, [i1*G + i2]
+    std::vector<double> thresholds; // G-1 cell-locate thresholds (lmkan_b200_thresholds)
+    double inv_area(int i1, int i2) const { return inv_areas[static_cast<std::size_t>(i1) * G + i2]; }
+};
+
+// grid.hpp:44-68 (throws std::invalid_argument for G < 3).
+inline SigmaGrid build_grid(int G) {
+    SigmaGrid g;
+    g.G = G;
+    g.points.assign(G >= 0 ? G + 1 : 0, 0.0);
+    g.inv_areas.assign(G > 0 ? static_cast<std::size_t>(G) * G : 0, 0.0);
+    detail::throw_status(lmkan_b200_build_grid(G, g.points.data(), g.inv_areas.data()), "build_grid");
+    g.thresholds.assign(G - 1, 0.0);
+    detail::throw_status(lmkan_b200_thresholds(G, g.thresholds.data(), nullptr), "build_grid");
+    return g;
+}
+
+// grid.hpp:72-75, bit-exact: #{k : x >= t_k} (NaN -> 0).
+inline int interval_index(const SigmaGrid& grid, double x) {
+    int i = 0;
+    for (double t : grid.thresholds) i += x >= t;
+    return i;
+}
+
+namespace detail {
+struct Prepared {
+    lmkan_b200_layer* h = nullptr;
+    int n_in = 0, n_out = 0, G = 0, device = 0;
+    std::uint64_t fingerprint = 0;
+    ~Prepared() {
+        if (h) lmkan_b200_layer_destroy(h);
+    }
+};
+
+inline std::uint64_t fingerprint(const std::vector<double>& P) {
+    // four independent multiply / xor-shift lanes over the raw 64-bit words
+    // (the xor-shift carries every bit, including sign flips, into later rounds)
+    const std::uint64_t k = 0x9e3779b97f4a7c15ull;
+    std::uint64_t a = 1, b = 2, c = 3, d = 4;
+    const std::size_t n = P.size();
+    std::size_t i = 0;
+    auto word = [&](std::size_t j) {
+        std::uint64_t u;
+        std::memcpy(&u, &P[j], 8);
+        return u;
+    };
+    auto mix = [&](std::uint64_t h, std::uint64_t w) {
+        h = (h ^ w) * k;
+        return h ^ (h >> 29);
+    };
+    for (; i + 4 <= n; i += 4) {
+        a = mix(a, word(i));
+        b = mix(b, word(i + 1));
+        c = mix(c, word(i + 2));
+        d = mix(d, word(i + 3));
+    }
+    for (; i < n; ++i) a = mix(a, word(i));
+    return mix(mix(mix(mix(n, a), b), c), d);
+}
+}  // namespace detail
+
+// layer.hpp:24-61. Same public fields and the same P layout
+// [i1][i2][pair][out] (out fastest); `device` selects the GPU.
+struct LmKanLayer {
+    int n_in = 0;
+    int n_out = 0;
+    SigmaGrid grid;
+    std::vector<double> P;
+    double gamma = 0.0;
+    int device = 0;
+
+    LmKanLayer() = default;
+    // Copies share no device state: a copied layer (whose P the caller may then
+    // edit) prepares its own table on first use.
+    LmKanLayer(const LmKanLayer& o)
+        : n_in(o.n_in), n_out(o.n_out), grid(o.grid), P(o.P), gamma(o.gamma), device(o.device) {}
+    LmKanLayer& operator=(const LmKanLayer& o) {
+        if (this != &o) {
+            n_in = o.n_in; n_out = o.n_out; grid = o.grid; P = o.P; gamma = o.gamma; device = o.device;
+            cache_.reset();
+            frozen_ = false;
+        }
+        return *this;
+    }
+    LmKanLayer(LmKanLayer&&) = default;
+    LmKanLayer& operator=(LmKanLayer&&) = default;
+
+    int pairs() const { return n_in / 2; }
+    std::size_t param_count() const { return P.size(); }
+    std::size_t node_offset(int i1, int i2) const {
+        const std::size_t per_node = static_cast<std::size_t>(pairs()) * n_out;
+        return (static_cast<std::size_t>(i1) * (grid.G + 1) + i2) * per_node;
+    }
+    double* node_slice(int i1, int i2, int pair) {
+        return P.data() + node_offset(i1, i2) + static_cast<std::size_t>(pair) * n_out;
+    }
+    const double* node_slice(int i1, int i2, int pair) const {
+        return P.data() + node_offset(i1, i2) + static_cast<std::size_t>(pair) * n_out;
+    }
+
+    // Promise that P will not change any more: forward skips the fingerprint.
+    void freeze() { frozen_ = true; }
+    // Drop the device table (e.g. to free GPU memory); rebuilt on next use.
+    void release() const { cache_.reset(); }
+
+    // The prepared device handle, (re)built if P changed since the last call.
+    lmkan_b200_layer* prepared() const {
+        const std::uint64_t fp = (frozen_ && cache_) ? cache_->fingerprint : detail::fingerprint(P);
+        if (!cache_ || cache_->fingerprint != fp || cache_->n_in != n_in || cache_->n_out != n_out ||
+            cache_->G != grid.G || cache_->device != device) {
+            auto pr = std::make_shared<detail::Prepared>();
+            detail::throw_status(
+                lmkan_b200_layer_create(n_in, n_out, grid.G, gamma, P.data(), device, &pr->h), "lmkan_forward");
+            pr->n_in = n_in; pr->n_out = n_out; pr->G = grid.G; pr->device = device;
+            pr->fingerprint = fp;
+            cache_ = std::move(pr);
+        }
+        detail::throw_status(lmkan_b200_layer_set_gamma(cache_->h, gamma), "lmkan_forward");
+        return cache_->h;
+    }
+
+private:
+    mutable std::shared_ptr<detail::Prepared> cache_;
+    bool frozen_ = false;
+};
+
+// layer.hpp:63-65
+inline double default_init_scale(int n_in) { return 1.0 / std::sqrt(static_cast<double>(n_in / 2)); }
+
+// layer.hpp:69-86: same validation, the same N(0, scale^2) table drawn from the
+// same named stream (bit-identical), gamma = 0.
+inline LmKanLayer init_layer(int n_in, int n_out, int G, std::uint64_t seed, double init_scale = -1.0) {
+    if (n_in <= 0 || n_in % 2 != 0) throw std::invalid_argument("init_layer: n_in must be a positive even number");
+    if (n_out <= 0) throw std::invalid_argument("init_layer: n_out must be positive");
+    LmKanLayer layer;
+    layer.n_in = n_in;
+    layer.n_out = n_out;
+    layer.grid = build_grid(G);
+    layer.P.assign(static_cast<std::size_t>(G + 1) * (G + 1) * (n_in / 2) * n_out, 0.0);
+    detail::throw_status(lmkan_b200_init_table(n_in, n_out, G, seed, init_scale, layer.P.data()), "init_layer");
+    layer.gamma = 0.0;
+    return layer;
+}
+
+// layer.hpp:108-134. Y is resized when its shape differs (layer.hpp:111-112).
+// `workers` is accepted for signature compatibility and ignored (the GPU
+// replaces the std::thread row split of threading.hpp:24-42). Blocks until Y
+// holds the result.
+inline void lmkan_forward(const LmKanLayer& layer, const Matrix& X, Matrix& Y, std::size_t workers = 0) {
+    require_width(X, layer.n_in, "lmkan_forward");
+    if (Y.rows() != X.rows() || Y.cols() != static_cast<std::size_t>(layer.n_out)) Y = Matrix(X.rows(), layer.n_out);
+    if (X.rows() == 0) return;
+    lmkan_b200_layer* h = layer.prepared();
+    detail::throw_status(lmkan_b200_forward_host_f64(h, X.data(), Y.data(), static_cast<std::int64_t>(X.rows()),
+                                                     workers),
+                         "lmkan_forward");
+}
+
+// Adapter for code that keeps the REFERENCE's own types (lmkan::LmKanLayer,
+// lmkan::Matrix): duck-typed on their public members, prepares a device table
+// per call (use LmKanLayer above to keep it resident).
+template <class RefLayer, class RefMatrix>
+void lmkan_forward_ref_types(const RefLayer& layer, const RefMatrix& X, RefMatrix& Y, int device = 0) {
+    if (X.cols() != static_cast<std::size_t>(layer.n_in))
+        throw std::invalid_argument("lmkan_forward: expected width " + std::to_string(layer.n_in) + ", got " +
+                                    std::to_string(X.cols()));
+    if (Y.rows() != X.rows() || Y.cols() != static_cast<std::size_t>(layer.n_out)) Y = RefMatrix(X.rows(), layer.n_out);
+    if (X.rows() == 0) return;
+    detail::Prepared pr;
+    detail::throw_status(
+        lmkan_b200_layer_create(layer.n_in, layer.n_out, layer.grid.G, layer.gamma, layer.P.data(), device, &pr.h),
+        "lmkan_forward");
+    detail::throw_status(lmkan_b200_forward_host_f64(pr.h, X.data(), Y.data(), static_cast<std::int64_t>(X.rows()), 0),
+                         "lmkan_forward");
+}
+
+}  // namespace lmkan_b200

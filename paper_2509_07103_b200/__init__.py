@@ -200,10 +200,12 @@ class Layer:
         return out
 
     def plan(self, rows: int) -> dict:
-        v = [C.c_int() for _ in range(5)]
+        v = [C.c_int() for _ in range(6)]
         check(lib.lmkan_b200_plan(self._h, int(rows), *[C.byref(x) for x in v]))
-        return dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches"],
-                        [x.value for x in v]))
+        d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode"],
+                     [x.value for x in v]))
+        d["mode"] = {0: "fused", 1: "staged", 2: "global"}[d["mode"]]
+        return d
 
     def close(self) -> None:
         if getattr(self, "_h", None):

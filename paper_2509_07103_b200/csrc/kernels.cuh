@@ -7,14 +7,17 @@
 //            (layer.hpp:116-133)
 //
 // Kernels:
-//   locate_kernel     K1: stage 1 alone -> (i1, i2, 4 fp32 weights) per (row, pair)
-//   fwd_fused_kernel  K3: stage 1 + stage 2 in one kernel. A CTA owns a tile of R
-//                     rows x OT outputs in registers and walks the pairs; per pair
-//                     the (G+1)^2 x OT coefficient sheet is streamed into shared
-//                     memory by the bulk-copy engine (cp.async.bulk + mbarrier,
-//                     NBUF-deep ring) while the CTA locates the next pair's cells
-//                     for its R rows into a shared-memory record ring. Warps then
-//                     gather float4 runs of the 4 corner rows of each row's cell.
+//   locate_kernel     stage 1 alone -> (i1, i2, 4 fp32 weights) per (row, pair)
+//                     (the parity/debug entry point lmkan_b200_locate_*)
+//   records_kernel    K1: stage 1 for the staged path -> cell records laid out
+//                     pair-major in exactly the order K2's warps consume them
+//   fwd_fused_kernel  K2 (MODE staged): gather-accumulate; per pair the CTA's
+//                     (G+1)^2 x OT coefficient sheet and its R cell records are
+//                     streamed into shared memory by the bulk-copy engine
+//                     (cp.async.bulk + mbarrier ring), warps gather float4 runs of
+//                     the 4 corner nodes and accumulate R x OT in registers.
+//                     K3 (MODE fused): same, cells located in-kernel per warp.
+//                     MODE global: fallback reading sheets from L2 (huge G).
 //   relayout / fill   one-time table preparation into [out_tile][pair][node][OT].
 #pragma once
 
@@ -65,6 +68,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -147,85 +155,253 @@ __global__ void __launch_bounds__(256) locate_kernel(const XT* __restrict__ X, i
     }
 }
 
-// Shared-memory carve-up of the fused kernel (host and device agree on it).
-struct FusedSmem {
-    uint32_t sheet_bytes, off_recw, off_reco, off_thr, off_pts, off_bar, total;
+// Fast cell index: an fp32 sigma estimate (MUFU exp) is corrected by one
+// threshold step either way and then VERIFIED against the threshold table
+// (t_k = thr[k-1]); only if the verification fails (NaN, or an estimate off by
+// more than one cell) does it fall back to the exact binary search. The result
+// is therefore always #{k : x >= t_k}, i.e. the reference interval_index.
+template <typename XT>
+__device__ __forceinline__ int cell_index_fast(XT x, const XT* thr, int G, int L) {
+    const float xf = static_cast<float>(x);
+    const float e = __expf(-fabsf(xf));
+    const float s = xf > 0.f ? 1.f - 0.5f * e : 0.5f * e;
+    int i = static_cast<int>(s * static_cast<float>(G));
+    i = i < 0 ? 0 : (i > G - 1 ? G - 1 : i);
+    if (i > 0 && !(x >= thr[i - 1])) --i;
+    else if (i < G - 1 && x >= thr[i]) ++i;
+    const bool ok = (i == 0 || x >= thr[i - 1]) && (i == G - 1 || x < thr[i]);
+    return ok ? i : cell_index<XT>(x, thr, L);
+}
+
+// preamble weights (grid.hpp:91-99) from grid constants held in shared memory.
+template <typename XT>
+__device__ __forceinline__ int locate_record(XT x1, XT x2, const XT* thr, const double* pts, const double* inv,
+                                             int G, int L, float4& w) {
+    const int i1 = cell_index_fast<XT>(x1, thr, G, L);
+    const int i2 = cell_index_fast<XT>(x2, thr, G, L);
+    const double d1 = static_cast<double>(x1), d2 = static_cast<double>(x2);
+    const double a = __dsub_rn(pts[i1 + 1], d1);
+    const double b = __dsub_rn(d1, pts[i1]);
+    const double c = __dsub_rn(pts[i2 + 1], d2);
+    const double d = __dsub_rn(d2, pts[i2]);
+    const double iv = inv[i1 * G + i2];
+    w.x = __double2float_rn(__dmul_rn(__dmul_rn(a, c), iv));
+    w.y = __double2float_rn(__dmul_rn(__dmul_rn(b, c), iv));
+    w.z = __double2float_rn(__dmul_rn(__dmul_rn(a, d), iv));
+    w.w = __double2float_rn(__dmul_rn(__dmul_rn(b, d), iv));
+    return i1 * (G + 1) + i2;
+}
+
+// Kernel variants of the layer forward.
+enum : int {
+    kModeFused = 0,   // K3: cells located in-kernel (warp-local), sheets via bulk copy
+    kModeStaged = 1,  // K2: cell records produced by K1 (records_kernel), sheets + records via bulk copy
+    kModeGlobal = 2,  // fallback for sheets larger than shared memory: in-kernel locate, sheets read from L2
 };
-__host__ __device__ inline FusedSmem fused_smem_layout(int nodes, int OT, int R, int nbuf) {
+
+// Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
+template <int OT, int RT>
+struct FusedShape {
+    static constexpr int LPR = OT / 4;               // lanes covering one row's OT outputs (float4 each)
+    static constexpr int RPW = 32 / LPR;             // rows per warp per gather instruction
+    static constexpr int ROWS_W = RPW * RT;          // rows owned by one warp
+    static constexpr int LOC = (ROWS_W + 31) / 32;   // cells each lane locates per pair (fused mode)
+    static constexpr int R = kWarps * ROWS_W;        // rows per CTA
+    static constexpr int OSTRIDE = RT + (RPW > 2 ? 4 : 0);  // padded per-lane-group offset run (bank spread)
+    static constexpr int OBLK = kWarps * RPW * OSTRIDE;     // offset ints per CTA per pair
+};
+// Runtime twin of FusedShape for host code / K1.
+struct ShapeRT {
+    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK;
+};
+__host__ __device__ inline ShapeRT shape_rt(int OT, int RT) {
+    ShapeRT s;
+    s.OT = OT;
+    s.RT = RT;
+    s.LPR = OT / 4;
+    s.RPW = 32 / s.LPR;
+    s.ROWS_W = s.RPW * RT;
+    s.R = kWarps * s.ROWS_W;
+    s.OSTRIDE = RT + (s.RPW > 2 ? 4 : 0);
+    s.OBLK = kWarps * s.RPW * s.OSTRIDE;
+    return s;
+}
+// Position of CTA-local row qc's node offset inside the CTA's offset block: the
+// RT rows a lane group gathers are contiguous, so a thread loads them as int4s.
+__host__ __device__ inline int offset_slot(const ShapeRT& s, int qc) {
+    const int warp = qc / s.ROWS_W, q = qc % s.ROWS_W;
+    const int sub = q % s.RPW, j = q / s.RPW;
+    return (warp * s.RPW + sub) * s.OSTRIDE + j;
+}
+
+// Shared-memory carve-up (host and device agree on it).
+//   sheets : NBUF x (G+1)^2 x OT fp32 (bulk-copy destinations), not in global mode
+//   records: NREC x {R float4 weights, OBLK int node offsets}; NREC = NBUF when
+//            staged (they arrive with the sheet), else 1 (warp-private, in-kernel)
+//   grid constants (not staged): thresholds, points[G+1], inv_areas[G*G] (fp64)
+//   NBUF "landed" mbarriers + NBUF finished-warp counters
+struct FusedSmem {
+    uint32_t sheet_bytes, recw_bytes, reco_bytes, off_recw, off_reco, off_thr, off_pts, off_inv, off_bar,
+        off_cnt, total;
+};
+__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode) {
+    const ShapeRT sh = shape_rt(OT, RT);
+    const int nodes = (G + 1) * (G + 1);
+    const int nb = nbuf > 0 ? nbuf : 1;
+    const int nrec = mode == kModeStaged ? nb : 1;
     FusedSmem s;
     s.sheet_bytes = static_cast<uint32_t>(nodes) * OT * 4u;
-    uint32_t o = s.sheet_bytes * nbuf;
+    s.recw_bytes = sh.R * 16u;
+    s.reco_bytes = sh.OBLK * 4u;
+    uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
+    o = (o + 127u) & ~127u;
     s.off_recw = o;
-    o += 2u * R * 16u;
+    o += nrec * s.recw_bytes;
     s.off_reco = o;
-    o += 2u * R * 4u;
+    o += nrec * s.reco_bytes;
     o = (o + 15u) & ~15u;
     s.off_thr = o;
-    o += kMaxThr * 8u;
     s.off_pts = o;
-    o += (kMaxThr + 1) * 8u;
-    o = (o + 15u) & ~15u;
+    s.off_inv = o;
+    if (mode != kModeStaged) {
+        o += kMaxThr * 8u;
+        s.off_pts = o;
+        o += (kMaxThr + 1) * 8u;
+        o = (o + 15u) & ~15u;
+        s.off_inv = o;
+        o += static_cast<uint32_t>(G) * G * 8u;
+        o = (o + 15u) & ~15u;
+    }
     s.off_bar = o;
-    o += 8u * nbuf;
+    o += 8u * nb;
+    s.off_cnt = o;
+    o += 4u * nb;
     s.total = (o + 127u) & ~127u;
     return s;
 }
 
-template <int OT, int RT>
-struct FusedShape {
-    static constexpr int LPR = OT / 4;           // lanes covering one row's OT outputs (float4 each)
-    static constexpr int RPW = 32 / LPR;         // rows per warp per instruction
-    static constexpr int R = kWarps * RPW * RT;  // rows per CTA
-};
+// K1 (staged path): cell records for every (pair, row) in the order K2 consumes
+// them. A CTA stages a 64-row x 16-pair X tile through shared memory (row-
+// contiguous 128-B loads), locates each (row, pair) and writes
+//   W[p][row]                        = {w00, w10, w01, w11}      (coalesced)
+//   O[p][tile][offset_slot(row % R)] = node * OT                 (node offset in floats)
+// Rows in [rows, rows_pad) get zero records (their outputs are discarded).
+template <typename XT>
+__global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
+                                                      int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
+                                                      float4* __restrict__ W, int* __restrict__ O) {
+    __shared__ XT xs[64][33];
+    __shared__ XT thr[kMaxThr];
+    __shared__ double pts[kMaxThr + 1];
+    extern __shared__ double inv[];  // G*G
+    const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
+    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
+    for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int p0 = blockIdx.y * 16;
+    for (int i = tid; i < 64 * 32; i += 256) {
+        const int r = i >> 5, c = i & 31;
+        const int64_t g = r0 + r;
+        const int col = 2 * p0 + c;
+        xs[r][c] = (g < rows && col < n_in) ? X[g * n_in + col] : XT(0);
+    }
+    __syncthreads();
+    const int64_t tiles = rows_pad / sh.R;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int idx = tid + 256 * k;
+        const int r = idx & 63, pl = idx >> 6;
+        const int p = p0 + pl;
+        if (p >= pairs) continue;
+        const int64_t g = r0 + r;
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        int node = 0;
+        if (g < rows) node = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, w);
+        W[static_cast<size_t>(p) * rows_pad + g] = w;
+        const int64_t tile = g / sh.R;
+        const int qc = static_cast<int>(g - tile * sh.R);
+        O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = node * sh.OT;
+    }
+}
 
-// K3: fused locate + gather-accumulate. Grid: x = row tile (R rows), y = output
-// tile (OT outputs). Table layout [out_tile][pair][node][OT] fp32, so the sheet of
-// one (out_tile, pair) is one contiguous (G+1)^2*OT*4-byte bulk copy and each
-// node's OT outputs are a contiguous, float4-aligned run.
+// K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
+// Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
+// [out_tile][pair][node][OT] fp32: the sheet of one (out_tile, pair) is one
+// contiguous (G+1)^2*OT*4-byte bulk copy and each node's OT outputs are a
+// contiguous, float4-aligned run.
+//
+// Pipeline (no CTA-wide barrier inside the pair loop):
+//   * sheets (+ records when staged): NBUF-deep ring in shared memory filled by
+//     the bulk-copy engine; "full[s]" mbarriers count the landed bytes. The LAST
+//     warp to finish with a slot (shared-memory atomic counter) issues the copy
+//     that refills it, so no warp waits on a producer and none is dedicated.
+//   * fused mode: every warp locates the cells of its own rows for the next pair
+//     into a warp-private record slice (x pair prefetched a pair ahead).
+//   * gather: lane group `sub` handles one row, lane c4 a float4 of outputs; per
+//     row one LDS.128 of weights and 4 LDS.128 of coefficients (nodes n, n+1,
+//     n+G+1, n+G+2), 16 FMAs; node offsets of a lane group's RT rows are
+//     contiguous (int4 loads).
 //
 // Accumulation order per (row, output): acc = 0; for p: acc += t_p with
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
-// Deterministic: no atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT>
+// Deterministic: no data atomics, fixed order, independent of the launch shape.
+template <int OT, int RT, typename XT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, float gamma,
-                     const __grid_constant__ GridConst gc) {
+                     const __grid_constant__ GridConst gc, const float4* __restrict__ recW,
+                     const int* __restrict__ recO, int64_t rows_pad) {
     using S = FusedShape<OT, RT>;
     constexpr int R = S::R;
+    constexpr bool kSmemSheet = MODE != kModeGlobal;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
-    const FusedSmem L = fused_smem_layout(nodes, OT, R, nbuf);
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE);
     float* sheets = reinterpret_cast<float*>(smem);
     float4* rec_w = reinterpret_cast<float4*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
     XT* thr = reinterpret_cast<XT*>(smem + L.off_thr);
     double* pts = reinterpret_cast<double*>(smem + L.off_pts);
+    double* inv = reinterpret_cast<double*>(smem + L.off_inv);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+    unsigned* cnt = reinterpret_cast<unsigned*>(smem + L.off_cnt);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int sub = lane / S::LPR, c4 = lane % S::LPR;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * R;
+    const int64_t tile = blockIdx.x;
+    const int64_t row0 = tile * R;
     const int ot = blockIdx.y;
     const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
     const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * OT;
+    const int64_t tiles = rows_pad / R;
 
-    for (int k = tid; k < kMaxThr; k += kThreads) thr[k] = thr_of<XT>(gc)[k];
-    for (int k = tid; k <= G; k += kThreads) pts[k] = gc.points[k];
-    uint64_t policy = 0;
-    if (tid == 0) {
-        for (int s = 0; s < nbuf; ++s) mbar_init(&full[s], 1);
-        fence_barrier_init();
+    if constexpr (MODE != kModeStaged) {
+        for (int k = tid; k < kMaxThr; k += kThreads) thr[k] = thr_of<XT>(gc)[k];
+        for (int k = tid; k <= G; k += kThreads) pts[k] = gc.points[k];
+        for (int k = tid; k < G * G; k += kThreads) inv[k] = gc.inv_areas[k];
+    }
+    uint64_t policy = 0, policy_rec = 0;
+    if constexpr (kSmemSheet) {
+        if (tid == 0) {
+            for (int s = 0; s < nbuf; ++s) {
+                mbar_init(&full[s], 1);
+                cnt[s] = 0;
+            }
+            fence_barrier_init();
+        }
         policy = policy_evict_last();
+        policy_rec = policy_evict_first();
     }
     __syncthreads();
 
-    auto issue_sheet = [&](int p) {  // tid 0 only
+    auto issue = [&](int p) {  // one thread: sheet (+ records) of pair p into slot p % nbuf
         const int s = p % nbuf;
-        mbar_arrive_expect_tx(&full[s], L.sheet_bytes);
+        const uint32_t rec_bytes = MODE == kModeStaged ? L.recw_bytes + L.reco_bytes : 0u;
+        mbar_arrive_expect_tx(&full[s], L.sheet_bytes + rec_bytes);
         const char* src = reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * sheet_floats);
         char* dst = reinterpret_cast<char*>(sheets) + static_cast<size_t>(s) * L.sheet_bytes;
         constexpr uint32_t kChunk = 32768;
@@ -233,25 +409,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t n = L.sheet_bytes - o < kChunk ? L.sheet_bytes - o : kChunk;
             bulk_g2s(dst + o, src + o, n, &full[s], policy);
         }
+        if constexpr (MODE == kModeStaged) {
+            bulk_g2s(reinterpret_cast<char*>(rec_w) + s * L.recw_bytes,
+                     recW + static_cast<size_t>(p) * rows_pad + row0, L.recw_bytes, &full[s], policy_rec);
+            bulk_g2s(reinterpret_cast<char*>(rec_o) + s * L.reco_bytes,
+                     recO + (static_cast<size_t>(p) * tiles + tile) * S::OBLK, L.reco_bytes, &full[s], policy_rec);
+        }
     };
-    if (tid == 0) {
-        const int pre = nbuf < pairs ? nbuf : pairs;
-        for (int p = 0; p < pre; ++p) issue_sheet(p);
+    if constexpr (kSmemSheet) {
+        if (tid == 0) {
+            const int pre = nbuf < pairs ? nbuf : pairs;
+            for (int p = 0; p < pre; ++p) issue(p);
+        }
     }
 
-    auto locate = [&](int p, int buf) {
-        for (int i = tid; i < R; i += kThreads) {
-            const int64_t r = row0 + i;
-            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-            int off = 0;
-            if (r < rows) {
-                const XT* xr = X + r * n_in + 2 * p;
-                int i1, i2;
-                locate_pair<XT>(xr[0], xr[1], thr, pts, gc.inv_areas, G, gc.L, i1, i2, w);
-                off = (i1 * (G + 1) + i2) * OT;
+    // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane
+    XT xa[S::LOC], xb[S::LOC];
+    const XT* xrow[S::LOC];
+    const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0;
+#pragma unroll
+    for (int k = 0; k < S::LOC; ++k) {
+        const int q = k * 32 + lane;
+        const int64_t r = row0 + warp * S::ROWS_W + q;
+        xrow[k] = (MODE != kModeStaged && q < S::ROWS_W && r < rows) ? X + r * n_in : nullptr;
+    }
+    auto prefetch = [&](int p) {
+#pragma unroll
+        for (int k = 0; k < S::LOC; ++k) {
+            if (xrow[k]) {
+                if (sizeof(XT) == 4 && x_vec_ok) {
+                    const float2 v = __ldg(reinterpret_cast<const float2*>(xrow[k] + 2 * p));
+                    xa[k] = v.x;
+                    xb[k] = v.y;
+                } else {
+                    xa[k] = __ldg(xrow[k] + 2 * p);
+                    xb[k] = __ldg(xrow[k] + 2 * p + 1);
+                }
+            } else {
+                xa[k] = xb[k] = XT(0);
             }
-            rec_w[buf * R + i] = w;
-            rec_o[buf * R + i] = off;
+        }
+    };
+    auto locate = [&]() {
+        const ShapeRT sh = shape_rt(OT, RT);
+#pragma unroll
+        for (int k = 0; k < S::LOC; ++k) {
+            const int q = k * 32 + lane;
+            if (q < S::ROWS_W) {
+                float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+                int node = 0;
+                if (xrow[k]) node = locate_record<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, w);
+                const int qc = warp * S::ROWS_W + q;
+                rec_w[qc] = w;
+                rec_o[offset_slot(sh, qc)] = node * OT;
+            }
         }
     };
 
@@ -260,47 +471,92 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < RT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int rstride = (G + 1) * OT;  // node (i1+1, i2) is (G+1) nodes further
 
-    locate(0, 0);
-    __syncthreads();
+    if constexpr (MODE != kModeStaged) {
+        prefetch(0);
+        locate();
+        if (pairs > 1) prefetch(1);
+        __syncwarp();
+    }
     for (int p = 0; p < pairs; ++p) {
-        if (p + 1 < pairs) locate(p + 1, (p + 1) & 1);
-        const int s = p % nbuf;
-        mbar_wait(&full[s], static_cast<uint32_t>((p / nbuf) & 1));
-        const float* sh = sheets + static_cast<size_t>(s) * sheet_floats + 4 * c4;
-        const float4* rw = rec_w + (p & 1) * R;
-        const int* ro = rec_o + (p & 1) * R;
+        const float* sh;
+        const float4* rw = rec_w + warp * S::ROWS_W + sub;
+        const int* ro = rec_o + (warp * S::RPW + sub) * S::OSTRIDE;
+        if constexpr (kSmemSheet) {
+            const int s = p % nbuf;
+            mbar_wait(&full[s], static_cast<uint32_t>((p / nbuf) & 1));
+            sh = sheets + static_cast<size_t>(s) * sheet_floats + 4 * c4;
+            if constexpr (MODE == kModeStaged) {
+                rw += s * (L.recw_bytes / 16);
+                ro += s * (L.reco_bytes / 4);
+            }
+        } else {
+            sh = tsrc + static_cast<size_t>(p) * sheet_floats + 4 * c4;
+        }
+        int offs[RT];
+#pragma unroll
+        for (int k = 0; k < RT / 4; ++k) {
+            const int4 v = reinterpret_cast<const int4*>(ro)[k];
+            offs[4 * k] = v.x;
+            offs[4 * k + 1] = v.y;
+            offs[4 * k + 2] = v.z;
+            offs[4 * k + 3] = v.w;
+        }
 #pragma unroll
         for (int j = 0; j < RT; ++j) {
-            const int rl = (j * kWarps + warp) * S::RPW + sub;
-            const float4 w = rw[rl];
-            const float* b0 = sh + ro[rl];
+            const float4 w = rw[j * S::RPW];
+            const float* b0 = sh + offs[j];
             const float* b1 = b0 + rstride;
-            const float4 p00 = *reinterpret_cast<const float4*>(b0);
-            const float4 p01 = *reinterpret_cast<const float4*>(b0 + OT);
-            const float4 p10 = *reinterpret_cast<const float4*>(b1);
-            const float4 p11 = *reinterpret_cast<const float4*>(b1 + OT);
+            float4 p00, p01, p10, p11;
+            if constexpr (kSmemSheet) {
+                p00 = *reinterpret_cast<const float4*>(b0);
+                p01 = *reinterpret_cast<const float4*>(b0 + OT);
+                p10 = *reinterpret_cast<const float4*>(b1);
+                p11 = *reinterpret_cast<const float4*>(b1 + OT);
+            } else {
+                p00 = __ldg(reinterpret_cast<const float4*>(b0));
+                p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
+                p10 = __ldg(reinterpret_cast<const float4*>(b1));
+                p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+            }
             acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
             acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
             acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
             acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
         }
-        __syncthreads();  // sheet slot s and record buffer (p&1) are free again
-        if (tid == 0 && p + nbuf < pairs) {
-            fence_proxy_async();
-            issue_sheet(p + nbuf);
+        __syncwarp();  // this warp is done with its records and with sheet slot s
+        if constexpr (kSmemSheet) {
+            if (lane == 0) {
+                const int s = p % nbuf;
+                __threadfence_block();
+                if (atomicAdd(&cnt[s], 1u) == kWarps - 1) {  // last warp out refills the slot
+                    cnt[s] = 0;
+                    if (p + nbuf < pairs) {
+                        fence_proxy_async();
+                        issue(p + nbuf);
+                    }
+                }
+            }
+        }
+        if constexpr (MODE != kModeStaged) {
+            if (p + 1 < pairs) {
+                locate();
+                if (p + 2 < pairs) prefetch(p + 2);
+                __syncwarp();
+            }
         }
     }
 
-    // epilogue: y *= gamma (layer.hpp:131), masked store of the R x OT tile
+    // epilogue: y *= gamma (layer.hpp:131), masked store of the warp's rows
     const int col = ot * OT + 4 * c4;
+    const bool y_vec_ok = (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (n_out & 3) == 0;
 #pragma unroll
     for (int j = 0; j < RT; ++j) {
-        const int64_t r = row0 + (j * kWarps + warp) * S::RPW + sub;
+        const int64_t r = row0 + warp * S::ROWS_W + j * S::RPW + sub;
         if (r >= rows) continue;
         const float v[4] = {acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma, acc[j].w * gamma};
         XT* yr = Y + r * n_out;
         if constexpr (sizeof(XT) == 4) {
-            if (col + 3 < n_out && (n_out & 3) == 0) {
+            if (col + 3 < n_out && y_vec_ok) {
                 *reinterpret_cast<float4*>(yr + col) = make_float4(v[0], v[1], v[2], v[3]);
                 continue;
             }

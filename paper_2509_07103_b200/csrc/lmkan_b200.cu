@@ -98,86 +98,107 @@ int max_smem_optin(int device) {
 
 // ---------------------------------------------------------------- planning
 struct Plan {
-    int OT, RT, nbuf, R;
+    int OT, RT, nbuf, mode;
+    ShapeRT sh;
     uint32_t smem;
-    int64_t row_tiles;
+    int64_t row_tiles, rows_pad;
+    int launches;
 };
 
 constexpr int kRTChoices[] = {16, 8, 4};
+constexpr int kNumSMs = 148;
 
-int rows_per_cta(int OT, int RT) { return kWarps * (32 / (OT / 4)) * RT; }
+int rows_per_cta(int OT, int RT) { return shape_rt(OT, RT).R; }
 
-// Output tile width for a layer: the widest of {128, 64, 32, 16} (not wider
-// than the padded layer) whose sheet can be double-buffered next to the
-// record rings at the largest row tile.
+// Output tile width for a layer: the widest of {64, 32, 16} (not padding a
+// small layer by 2x or more) whose sheet can be double-buffered in shared
+// memory at some row tile; else the narrowest that fits single-buffered.
 int choose_out_tile(int n_out, int G, int smem_cap) {
     if (const char* e = std::getenv("LMKAN_B200_OT")) {
         const int v = std::atoi(e);
         if (v == 16 || v == 32 || v == 64 || v == 128) return v;
     }
-    const int nodes = (G + 1) * (G + 1);
-    const int cands[] = {64, 32, 16};
-    for (int OT : cands) {
-        if (OT > 16 && OT / 2 >= n_out) continue;  // do not pad small layers 2x
-        for (int RT : kRTChoices) {
-            const FusedSmem s = fused_smem_layout(nodes, OT, rows_per_cta(OT, RT), 2);
-            if (static_cast<int>(s.total) <= smem_cap) return OT;
+    for (int want_buf : {2, 1}) {
+        for (int OT : {64, 32, 16}) {
+            if (OT > 16 && OT / 2 >= n_out) continue;
+            for (int RT : kRTChoices) {
+                const FusedSmem s = fused_smem_layout(G, OT, RT, want_buf, kModeStaged);
+                if (static_cast<int>(s.total) <= smem_cap) return OT;
+            }
         }
     }
     return 16;
 }
 
+// Mode: staged (K1 + K2) when several output tiles re-read the same cells (the
+// locate then runs once per (row, pair) instead of once per output tile and
+// the gather kernel's shared-memory port serves only gathers); fused (K3)
+// otherwise; global-sheet fallback when no sheet fits shared memory.
 bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
-    int force_rt = 0, force_nbuf = 0;
+    int force_rt = 0, force_nbuf = 0, force_mode = -1;
     if (const char* e = std::getenv("LMKAN_B200_RT")) force_rt = std::atoi(e);
     if (const char* e = std::getenv("LMKAN_B200_NBUF")) force_nbuf = std::atoi(e);
-    const int num_sms = 148;
-    bool found = false;
-    for (int RT : kRTChoices) {
-        if (force_rt && RT != force_rt) continue;
-        const int R = rows_per_cta(L->OT, RT);
-        const int64_t tiles = (rows + R - 1) / R;
-        // keep >= ~1 wave of CTAs when the batch allows it
-        if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < num_sms) continue;
-        for (int nbuf = 4; nbuf >= 1; --nbuf) {
-            if (force_nbuf && nbuf != force_nbuf) continue;
-            if (nbuf > L->pairs && nbuf > 1) continue;
-            const FusedSmem s = fused_smem_layout(L->nodes, L->OT, R, nbuf);
-            if (static_cast<int>(s.total) > smem_cap) continue;
-            out = Plan{L->OT, RT, nbuf, R, s.total, tiles};
-            found = true;
-            break;
-        }
-        if (found) break;
+    if (const char* e = std::getenv("LMKAN_B200_MODE")) {
+        if (!std::strcmp(e, "fused")) force_mode = kModeFused;
+        if (!std::strcmp(e, "staged")) force_mode = kModeStaged;
+        if (!std::strcmp(e, "global")) force_mode = kModeGlobal;
     }
-    return found;
+    const int pref = L->n_ot >= 3 ? kModeStaged : kModeFused;
+    const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
+    for (int mode : modes) {
+        if (force_mode >= 0 && mode != force_mode) continue;
+        for (int RT : kRTChoices) {
+            if (force_rt && RT != force_rt) continue;
+            const ShapeRT sh = shape_rt(L->OT, RT);
+            const int64_t tiles = (rows + sh.R - 1) / sh.R;
+            // prefer the largest row tile that still gives >= one wave of CTAs
+            if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
+            const bool smem_sheet = mode != kModeGlobal;
+            for (int nbuf = smem_sheet ? 4 : 0; nbuf >= (smem_sheet ? 1 : 0); --nbuf) {
+                if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
+                if (smem_sheet && nbuf > L->pairs && nbuf > 1) continue;
+                const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode);
+                if (static_cast<int>(s.total) > smem_cap) continue;
+                out = Plan{L->OT, RT, nbuf, mode, sh, s.total, tiles, tiles * sh.R, mode == kModeStaged ? 2 : 1};
+                return true;
+            }
+        }
+    }
+    return false;
 }
 
-template <int OT, int RT, typename XT>
+template <int OT, int RT, typename XT, int MODE>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                           cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT>;
-    static thread_local int configured_smem[64] = {0};
-    const int dev = L->device;
-    if (configured_smem[dev & 63] < static_cast<int>(pl.smem)) {
+                           const float4* recW, const int* recO, cudaStream_t st) {
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE>;
+    static int configured[64] = {0};  // per device: dynamic-smem opt-in done
+    const int dev = L->device & 63;
+    if (!configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return e;
-        configured_smem[dev & 63] = 232448;
+        configured[dev] = 1;
     }
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
     kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf,
-                                           static_cast<float>(L->gamma), L->gc);
+                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad);
     return cudaGetLastError();
 }
 
 template <int OT, typename XT>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                            cudaStream_t st) {
-    switch (pl.RT) {
-        case 16: return launch_fused_t<OT, 16, XT>(L, pl, X, Y, rows, st);
-        case 8: return launch_fused_t<OT, 8, XT>(L, pl, X, Y, rows, st);
-        default: return launch_fused_t<OT, 4, XT>(L, pl, X, Y, rows, st);
+                            const float4* recW, const int* recO, cudaStream_t st) {
+    if (pl.mode == kModeGlobal) return launch_fused_t<OT, 4, XT, kModeGlobal>(L, pl, X, Y, rows, recW, recO, st);
+#define LMKAN_RT_CASES(MODE)                                                                        \
+    switch (pl.RT) {                                                                                \
+        case 16: return launch_fused_t<OT, 16, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);        \
+        case 8: return launch_fused_t<OT, 8, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);          \
+        default: return launch_fused_t<OT, 4, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);         \
     }
+    if (pl.mode == kModeStaged) {
+        LMKAN_RT_CASES(kModeStaged)
+    }
+    LMKAN_RT_CASES(kModeFused)
+#undef LMKAN_RT_CASES
 }
 
 template <typename XT>
@@ -186,21 +207,45 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
     if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
     if (rows == 0) return LMKAN_B200_OK;
     if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
-    if (reinterpret_cast<uintptr_t>(Y) % 16 != 0)
-        return fail(LMKAN_B200_EINVAL, "lmkan_forward: Y must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(Y) % sizeof(XT) != 0 || reinterpret_cast<uintptr_t>(X) % sizeof(XT) != 0)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: X and Y must be aligned to their element size");
     DeviceGuard g(L->device);
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory (G too large)");
     if (pl.row_tiles > 0x7fffffff) return fail(LMKAN_B200_EINVAL, "lmkan_forward: batch too large");
+    float4* recW = nullptr;
+    int* recO = nullptr;
+    if (pl.mode == kModeStaged) {
+        // K1: cell records, stream-ordered scratch (pool memory is retained, see alloc_layer)
+        const size_t wbytes = static_cast<size_t>(L->pairs) * pl.rows_pad * sizeof(float4);
+        const size_t obytes = static_cast<size_t>(L->pairs) * pl.row_tiles * pl.sh.OBLK * sizeof(int);
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&recW), wbytes, st));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&recO), obytes, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(recW, st);
+            return cuda_fail(e, "lmkan_forward: record scratch");
+        }
+        dim3 g1(static_cast<unsigned>(pl.rows_pad / 64), static_cast<unsigned>((L->pairs + 15) / 16));
+        records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
+                                                                            pl.sh, recW, recO);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            cudaFreeAsync(recW, st);
+            cudaFreeAsync(recO, st);
+            return cuda_fail(e, "lmkan_forward: records kernel launch");
+        }
+    }
     cudaError_t e;
     switch (L->OT) {
-        case 128: e = launch_fused_rt<128, XT>(L, pl, X, Y, rows, st); break;
-        case 64: e = launch_fused_rt<64, XT>(L, pl, X, Y, rows, st); break;
-        case 32: e = launch_fused_rt<32, XT>(L, pl, X, Y, rows, st); break;
-        default: e = launch_fused_rt<16, XT>(L, pl, X, Y, rows, st); break;
+        case 128: e = launch_fused_rt<128, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        case 64: e = launch_fused_rt<64, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        case 32: e = launch_fused_rt<32, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        default: e = launch_fused_rt<16, XT>(L, pl, X, Y, rows, recW, recO, st); break;
     }
-    if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: fused kernel launch");
+    if (recW) cudaFreeAsync(recW, st);
+    if (recO) cudaFreeAsync(recO, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: gather kernel launch");
     return LMKAN_B200_OK;
 }
 
@@ -276,6 +321,13 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
         return cuda_fail(e, "layer_create: device allocation");
     }
     gc.inv_areas = L->d_inv;
+    {  // keep stream-ordered scratch (cell records, host-path staging) in the pool between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     *out = L;
     return LMKAN_B200_OK;
 }
@@ -314,7 +366,7 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
-    const int64_t min_chunk = static_cast<int64_t>(pl.R) * 148 / std::max(1, L->n_ot);
+    const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * 148 / std::max(1, L->n_ot);
     int64_t chunk = std::max<int64_t>({(rows + 7) / 8, min_chunk, 1});
     chunk = std::min(chunk, rows);
     const size_t xb = static_cast<size_t>(chunk) * L->n_in * sizeof(XT);
@@ -516,15 +568,16 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i
 }
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
-                    int* rows_per_cta_out, int* launches) {
+                    int* rows_per_cta_out, int* launches, int* mode) {
     if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits");
     if (out_tile) *out_tile = pl.OT;
     if (rows_per_thread) *rows_per_thread = pl.RT;
     if (nbuf) *nbuf = pl.nbuf;
-    if (rows_per_cta_out) *rows_per_cta_out = pl.R;
-    if (launches) *launches = 1;
+    if (rows_per_cta_out) *rows_per_cta_out = pl.sh.R;
+    if (launches) *launches = pl.launches;
+    if (mode) *mode = pl.mode;
     return LMKAN_B200_OK;
 }
 

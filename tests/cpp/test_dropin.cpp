@@ -1,0 +1,188 @@
+// Drop-in test of the C++ host API (include/lmkan_b200/lmkan.hpp) on a GPU.
+// Mirrors the forward cases of the reference's test_layer.cpp (cited per case)
+// with the caller code unchanged apart from `namespace lmkan = lmkan_b200;`.
+// The fp64 oracles used here (dense O(G^2) basis sum, linear sheets) are
+// independent restatements in this file (func2d.hpp:32-73); tolerance is the
+// fp32 contract |d| <= 1e-5 * max(1, |ref|) instead of the reference's fp64 1e-12.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+
+#include "lmkan_b200/lmkan.hpp"
+
+namespace lmkan = lmkan_b200;
+using namespace lmkan;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                           \
+    do {                                                                   \
+        ++g_checks;                                                        \
+        if (!(c)) {                                                        \
+            ++g_fail;                                                      \
+            std::fprintf(stderr, "%s:%d CHECK failed: %s\n", __FILE__, __LINE__, #c); \
+        }                                                                  \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)        \
+    do {                                \
+        bool ok = false;                \
+        try {                           \
+            expr;                       \
+        } catch (const T&) {            \
+            ok = true;                  \
+        } catch (...) {                 \
+        }                               \
+        CHECK(ok);                      \
+    } while (0)
+
+static bool close_mixed(double y, double ref, double tol = 1e-5) {
+    return std::abs(y - ref) <= tol * std::max(1.0, std::abs(ref));
+}
+
+static Matrix random_batch(std::size_t rows, std::size_t cols, std::mt19937_64& g, double scale = 1.0) {
+    std::normal_distribution<double> n(0.0, 1.0);
+    Matrix X(rows, cols);
+    for (std::size_t i = 0; i < X.size(); ++i) X.data()[i] = scale * n(g);
+    return X;
+}
+
+// func2d.hpp:32-48 restated: hat function i at x, edge segments unbounded.
+static double basis_1d(const SigmaGrid& g, int i, double x) {
+    const int G = g.G;
+    const auto& p = g.points;
+    if (i == 0) return x < p[1] ? (p[1] - x) / (p[1] - p[0]) : 0.0;
+    if (i == G) return x > p[G - 1] ? (x - p[G - 1]) / (p[G] - p[G - 1]) : 0.0;
+    if (x < p[i]) return (i == 1 || x >= p[i - 1]) ? (x - p[i - 1]) / (p[i] - p[i - 1]) : 0.0;
+    return (i == G - 1 || x <= p[i + 1]) ? (p[i + 1] - x) / (p[i + 1] - p[i]) : 0.0;
+}
+
+// test_layer.cpp:20-32 restated: gamma * sum_p dense-oracle(sheet(p, q)).
+static Matrix dense_reference(const LmKanLayer& L, const Matrix& X) {
+    Matrix Y(X.rows(), L.n_out);
+    const int G = L.grid.G;
+    for (std::size_t r = 0; r < X.rows(); ++r)
+        for (int q = 0; q < L.n_out; ++q) {
+            double acc = 0.0;
+            for (int p = 0; p < L.pairs(); ++p)
+                for (int i1 = 0; i1 <= G; ++i1) {
+                    const double b1 = basis_1d(L.grid, i1, X(r, 2 * p));
+                    if (b1 == 0.0) continue;
+                    for (int i2 = 0; i2 <= G; ++i2)
+                        acc += L.node_slice(i1, i2, p)[q] * b1 * basis_1d(L.grid, i2, X(r, 2 * p + 1));
+                }
+            Y(r, q) = L.gamma * acc;
+        }
+    return Y;
+}
+
+static void test_init_layer() {  // test_layer.cpp:50-72
+    const LmKanLayer layer = init_layer(4, 3, 4, 123);
+    CHECK(layer.n_in == 4 && layer.n_out == 3);
+    CHECK(layer.P.size() == 5u * 5u * 2u * 3u);
+    CHECK(layer.gamma == 0.0);
+    CHECK(layer.P == init_layer(4, 3, 4, 123).P);
+    CHECK(layer.P != init_layer(4, 3, 4, 124).P);
+    LmKanLayer zero = init_layer(4, 3, 4, 1, 0.0);
+    zero.gamma = 1.0;
+    std::mt19937_64 g(9);
+    Matrix X = random_batch(16, 4, g), Y;
+    lmkan_forward(zero, X, Y);
+    for (std::size_t i = 0; i < Y.size(); ++i) CHECK(Y.data()[i] == 0.0);
+    CHECK_THROWS_AS(init_layer(3, 2, 4, 0), std::invalid_argument);
+    CHECK_THROWS_AS(init_layer(0, 2, 4, 0), std::invalid_argument);
+    CHECK_THROWS_AS(build_grid(2), std::invalid_argument);
+}
+
+static void test_dense_oracle() {  // test_layer.cpp:74-99
+    std::mt19937_64 g(11);
+    for (int G : {3, 5, 12}) {
+        LmKanLayer layer = init_layer(6, 5, G, 77 + G);
+        layer.gamma = 0.8;
+        const Matrix X = random_batch(64, 6, g, 1.5);
+        Matrix Y;
+        lmkan_forward(layer, X, Y);
+        const Matrix R = dense_reference(layer, X);
+        for (std::size_t i = 0; i < Y.size(); ++i) CHECK(close_mixed(Y.data()[i], R.data()[i]));
+    }
+}
+
+static void test_width_mismatch() {  // test_layer.cpp:101-110
+    LmKanLayer layer = init_layer(4, 2, 4, 5);
+    Matrix X(3, 6), Y;
+    CHECK_THROWS_AS(lmkan_forward(layer, X, Y), std::invalid_argument);
+    try {
+        lmkan_forward(layer, X, Y);
+    } catch (const std::invalid_argument& e) {
+        CHECK(std::string(e.what()) == "lmkan_forward: expected width 4, got 6");
+    }
+}
+
+static void test_linear_sheets() {  // test_layer.cpp:112-145
+    std::mt19937_64 g(12);
+    std::normal_distribution<double> n(0.0, 1.0);
+    LmKanLayer layer = init_layer(8, 3, 4, 99);
+    layer.gamma = 0.6;
+    double A[3][4], B[3][4], C[3][4];
+    for (int q = 0; q < 3; ++q)
+        for (int p = 0; p < 4; ++p) A[q][p] = n(g), B[q][p] = n(g), C[q][p] = n(g);
+    for (int p = 0; p < 4; ++p)
+        for (int q = 0; q < 3; ++q)
+            for (int i = 0; i <= 4; ++i)
+                for (int j = 0; j <= 4; ++j)
+                    layer.node_slice(i, j, p)[q] =
+                        A[q][p] * layer.grid.points[i] + B[q][p] * layer.grid.points[j] + C[q][p];
+    const Matrix X = random_batch(32, 8, g, 2.0);
+    Matrix Y;
+    lmkan_forward(layer, X, Y);
+    for (std::size_t r = 0; r < X.rows(); ++r)
+        for (int q = 0; q < 3; ++q) {
+            double want = 0.0;
+            for (int p = 0; p < 4; ++p) want += A[q][p] * X(r, 2 * p) + B[q][p] * X(r, 2 * p + 1) + C[q][p];
+            CHECK(close_mixed(Y(r, q), 0.6 * want));
+        }
+}
+
+static void test_determinism_and_cache() {  // test_layer.cpp:228-239 + P edits
+    LmKanLayer layer = init_layer(8, 6, 12, 2024);
+    layer.gamma = 0.9;
+    std::mt19937_64 g(15);
+    const Matrix X = random_batch(33, 8, g);
+    Matrix Y1, Y2;
+    lmkan_forward(layer, X, Y1);
+    lmkan_forward(layer, X, Y2);
+    for (std::size_t i = 0; i < Y1.size(); ++i) CHECK(Y1.data()[i] == Y2.data()[i]);
+    // finite-difference style edits on a copy (test_layer.cpp:198-205) see the edit
+    LmKanLayer bumped = layer;
+    for (double& v : bumped.P) v *= 2.0;
+    Matrix Yb;
+    lmkan_forward(bumped, X, Yb);
+    for (std::size_t i = 0; i < Y1.size(); ++i) CHECK(close_mixed(Yb.data()[i], 2.0 * Y1.data()[i]));
+    // in-place edit of the same layer
+    for (double& v : layer.P) v = -v;
+    lmkan_forward(layer, X, Y2);
+    for (std::size_t i = 0; i < Y1.size(); ++i) CHECK(close_mixed(Y2.data()[i], -Y1.data()[i]));
+    // gamma change only
+    layer.gamma = 0.0;
+    lmkan_forward(layer, X, Y2);
+    for (std::size_t i = 0; i < Y2.size(); ++i) CHECK(Y2.data()[i] == 0.0);
+}
+
+static void test_interval_index() {  // test_grid.cpp:108-114
+    const SigmaGrid g4 = build_grid(4);
+    CHECK(interval_index(g4, 0.1) == 2);
+    CHECK(interval_index(g4, -100.0) == 0);
+    CHECK(interval_index(g4, 100.0) == 3);
+    CHECK(interval_index(g4, 1e308) == 3);
+    CHECK(interval_index(g4, std::nan("")) == 0);
+}
+
+int main() {
+    test_init_layer();
+    test_dense_oracle();
+    test_width_mismatch();
+    test_linear_sheets();
+    test_determinism_and_cache();
+    test_interval_index();
+    std::printf("test_dropin: %d checks, %d failures\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}

@@ -1,0 +1,62 @@
+"""Kernel-variant sweep on one GPU (in-process; LMKAN_B200_* env vars are read
+per call). Usage: python tools/sweep.py [config] — prints one line per variant."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2509_07103_b200 as pkg  # noqa: E402
+
+
+def time_layer(layers, X, acts, iters=10):
+    s = torch.cuda.current_stream()
+
+    def step():
+        cur = X
+        for lay, out in zip(layers, acts):
+            lay.forward_into(cur, out, s)
+            cur = out
+    for _ in range(3):
+        step()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(s)
+    for _ in range(iters):
+        step()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    cfgn = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    cfg = bench.CONFIGS[cfgn]
+    variants = json.loads(os.environ.get("SWEEP", "[]")) or [
+        {"LMKAN_B200_MODE": m, "LMKAN_B200_RT": rt, "LMKAN_B200_NBUF": nb}
+        for m in ("staged", "fused") for rt in ("16", "8") for nb in ("2", "1", "3")]
+    G, B = cfg["G"], cfg["batch"]
+    X = torch.randn((B, cfg["layers"][0][0]), device="cuda")
+    acts = [torch.empty((B, o), device="cuda") for _, o in cfg["layers"]]
+    ot_cache = {}
+    for v in variants:
+        for k in ("LMKAN_B200_MODE", "LMKAN_B200_RT", "LMKAN_B200_NBUF", "LMKAN_B200_OT"):
+            os.environ.pop(k, None)
+        os.environ.update(v)
+        key = v.get("LMKAN_B200_OT", "")
+        if key not in ot_cache:
+            ot_cache[key] = [pkg.Layer.random(a, b, G, seed=1000 + i) for i, (a, b) in enumerate(cfg["layers"])]
+        layers = ot_cache[key]
+        try:
+            ms = time_layer(layers, X, acts)
+            plan = layers[0].plan(B)
+            print(json.dumps({"variant": v, "ms": round(ms, 4), "samples_per_s": B / ms * 1e3, "plan": plan}),
+                  flush=True)
+        except Exception as e:  # noqa: BLE001
+            print(json.dumps({"variant": v, "error": str(e)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
