@@ -109,6 +109,13 @@ int lmkan_b200_layer_destroy(lmkan_b200_layer* layer);
  * cell indices bit-exact, fp32 accumulation in the reference pair order. */
 int lmkan_b200_forward_f32(const lmkan_b200_layer* layer, const float* X_dev, float* Y_dev,
                            int64_t rows, void* stream);
+/* Profiling variant of lmkan_b200_forward_f32: additionally records the
+ * caller's CUDA events (cudaEvent_t, either may be NULL) on `stream` right
+ * before and right after the gather kernel, so the dominant kernel can be
+ * timed alone (bench.py's roofline). */
+int lmkan_b200_forward_f32_timed(const lmkan_b200_layer* layer, const float* X_dev, float* Y_dev,
+                                 int64_t rows, void* stream, void* ev_gather_begin,
+                                 void* ev_gather_end);
 /* Same, with fp64 inputs/outputs on the device (cells located in fp64 against
  * the fp64 thresholds, so indices stay bit-exact for any double X). */
 int lmkan_b200_forward_f64(const lmkan_b200_layer* layer, const double* X_dev, double* Y_dev,

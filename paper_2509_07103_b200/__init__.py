@@ -151,6 +151,11 @@ class Layer:
         fn = lib.lmkan_b200_forward_f32 if X.dtype == torch.float32 else lib.lmkan_b200_forward_f64
         check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream)))
 
+    def forward_into_timed(self, X, Y, ev_begin, ev_end, stream=None) -> None:
+        """forward_into (float32) recording torch.cuda.Events around the gather kernel."""
+        check(lib.lmkan_b200_forward_f32_timed(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream),
+                                               C.c_void_p(ev_begin.cuda_event), C.c_void_p(ev_end.cuda_event)))
+
     def forward(self, X, stream=None):
         """torch CUDA tensor in -> CUDA tensor out; numpy in -> numpy out (host path)."""
         if isinstance(X, np.ndarray):

@@ -202,7 +202,8 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
 }
 
 template <typename XT>
-int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
+                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr) {
     if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
     if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
     if (rows == 0) return LMKAN_B200_OK;
@@ -237,12 +238,14 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
         }
     }
     cudaError_t e;
+    if (ev_begin) cudaEventRecord(ev_begin, st);
     switch (L->OT) {
         case 128: e = launch_fused_rt<128, XT>(L, pl, X, Y, rows, recW, recO, st); break;
         case 64: e = launch_fused_rt<64, XT>(L, pl, X, Y, rows, recW, recO, st); break;
         case 32: e = launch_fused_rt<32, XT>(L, pl, X, Y, rows, recW, recO, st); break;
         default: e = launch_fused_rt<16, XT>(L, pl, X, Y, rows, recW, recO, st); break;
     }
+    if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
     if (recO) cudaFreeAsync(recO, st);
     if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: gather kernel launch");
@@ -546,6 +549,11 @@ int lmkan_b200_layer_destroy(lmkan_b200_layer* L) {
 
 int lmkan_b200_forward_f32(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, void* stream) {
     return forward_device<float>(L, X, Y, rows, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_forward_f32_timed(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, void* stream,
+                                 void* ev_begin, void* ev_end) {
+    return forward_device<float>(L, X, Y, rows, static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev_begin),
+                                 static_cast<cudaEvent_t>(ev_end));
 }
 int lmkan_b200_forward_f64(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, void* stream) {
     return forward_device<double>(L, X, Y, rows, static_cast<cudaStream_t>(stream));
