@@ -205,9 +205,9 @@ class Layer:
         return out
 
     def plan(self, rows: int) -> dict:
-        v = [C.c_int() for _ in range(6)]
+        v = [C.c_int() for _ in range(7)]
         check(lib.lmkan_b200_plan(self._h, int(rows), *[C.byref(x) for x in v]))
-        d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode"],
+        d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode", "slabs"],
                      [x.value for x in v]))
         d["mode"] = {0: "fused", 1: "staged", 2: "global"}[d["mode"]]
         return d

@@ -172,11 +172,26 @@ __device__ __forceinline__ int cell_index_fast(XT x, const XT* thr, int G, int L
     const bool ok = (i == 0 || x >= thr[i - 1]) && (i == G - 1 || x < thr[i]);
     return ok ? i : cell_index<XT>(x, thr, L);
 }
+// Slab split of a sheet along i1: slab s holds the node rows
+// i1 in [s*H, min(G, s*H + H)], so every cell with i1 in [s*H, s*H + H) has all
+// four corners inside slab s, and a slab is a contiguous byte range of the
+// [node][OT] sheet. S = 1 (H = G) is the unsplit sheet. Large-G sheets are cut
+// into slabs so that two of them fit in shared memory (double buffering).
+__host__ __device__ inline int slab_node_rows(int G, int H, int s) {
+    const int r = G + 1 - s * H;
+    return r < H + 1 ? r : H + 1;
+}
 
-// preamble weights (grid.hpp:91-99) from grid constants held in shared memory.
+// Packed record offset: (slab << 24) | (node-within-slab * OT).
+constexpr int kSlabShift = 24;
+constexpr int kOffMask = (1 << kSlabShift) - 1;
+
+// preamble (grid.hpp:87-101) from grid constants held in shared memory: cell
+// index (bit-exact, thresholds) and the four weights in fp64, reference order
+// (a*c*inv == (a*c)*inv), rounded to fp32. Returns the packed node offset.
 template <typename XT>
 __device__ __forceinline__ int locate_record(XT x1, XT x2, const XT* thr, const double* pts, const double* inv,
-                                             int G, int L, float4& w) {
+                                             int G, int L, int OT, int H, float4& w) {
     const int i1 = cell_index_fast<XT>(x1, thr, G, L);
     const int i2 = cell_index_fast<XT>(x2, thr, G, L);
     const double d1 = static_cast<double>(x1), d2 = static_cast<double>(x2);
@@ -189,7 +204,8 @@ __device__ __forceinline__ int locate_record(XT x1, XT x2, const XT* thr, const 
     w.y = __double2float_rn(__dmul_rn(__dmul_rn(b, c), iv));
     w.z = __double2float_rn(__dmul_rn(__dmul_rn(a, d), iv));
     w.w = __double2float_rn(__dmul_rn(__dmul_rn(b, d), iv));
-    return i1 * (G + 1) + i2;
+    const int s = i1 / H;
+    return (s << kSlabShift) | (((i1 - s * H) * (G + 1) + i2) * OT);
 }
 
 // Kernel variants of the layer forward.
@@ -234,31 +250,37 @@ __host__ __device__ inline int offset_slot(const ShapeRT& s, int qc) {
     return (warp * s.RPW + sub) * s.OSTRIDE + j;
 }
 
+// Record-ring depth of the staged mode: records of pair p arrive with its first
+// slab and must outlive its S slabs while up to NBUF units are in flight.
+__host__ __device__ inline int staged_nrec(int nbuf, int S) { return (nbuf - 1 + S - 1) / S + 1; }
+
 // Shared-memory carve-up (host and device agree on it).
-//   sheets : NBUF x (G+1)^2 x OT fp32 (bulk-copy destinations), not in global mode
-//   records: NREC x {R float4 weights, OBLK int node offsets}; NREC = NBUF when
-//            staged (they arrive with the sheet), else 1 (warp-private, in-kernel)
+//   sheets : NBUF x slab buffers of (H+1)(G+1) x OT fp32 (bulk-copy destinations)
+//   records: NREC x {R float4 weights, OBLK packed offsets}; NREC = staged_nrec
+//            when staged (they arrive with a pair's first slab), else 1
+//            (warp-private, written by the in-kernel locate)
 //   grid constants (not staged): thresholds, points[G+1], inv_areas[G*G] (fp64)
 //   NBUF "landed" mbarriers + NBUF finished-warp counters
 struct FusedSmem {
     uint32_t sheet_bytes, recw_bytes, reco_bytes, off_recw, off_reco, off_thr, off_pts, off_inv, off_bar,
         off_cnt, total;
+    int nrec;
 };
-__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode) {
+__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1) {
     const ShapeRT sh = shape_rt(OT, RT);
-    const int nodes = (G + 1) * (G + 1);
+    const int H = (G + S - 1) / S;
     const int nb = nbuf > 0 ? nbuf : 1;
-    const int nrec = mode == kModeStaged ? nb : 1;
     FusedSmem s;
-    s.sheet_bytes = static_cast<uint32_t>(nodes) * OT * 4u;
+    s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
+    s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * OT * 4u;
     s.recw_bytes = sh.R * 16u;
     s.reco_bytes = sh.OBLK * 4u;
     uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
     o = (o + 127u) & ~127u;
     s.off_recw = o;
-    o += nrec * s.recw_bytes;
+    o += s.nrec * s.recw_bytes;
     s.off_reco = o;
-    o += nrec * s.reco_bytes;
+    o += s.nrec * s.reco_bytes;
     o = (o + 15u) & ~15u;
     s.off_thr = o;
     s.off_pts = o;
@@ -282,14 +304,14 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
 
 // K1 (staged path): cell records for every (pair, row) in the order K2 consumes
 // them. A CTA stages a 64-row x 16-pair X tile through shared memory (row-
-// contiguous 128-B loads), locates each (row, pair) and writes
+// contiguous loads), locates each (row, pair) and writes
 //   W[p][row]                        = {w00, w10, w01, w11}      (coalesced)
-//   O[p][tile][offset_slot(row % R)] = node * OT                 (node offset in floats)
+//   O[p][tile][offset_slot(row % R)] = packed slab / node offset
 // Rows in [rows, rows_pad) get zero records (their outputs are discarded).
 template <typename XT>
 __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
-                                                      float4* __restrict__ W, int* __restrict__ O) {
+                                                      int H, float4* __restrict__ W, int* __restrict__ O) {
     __shared__ XT xs[64][33];
     __shared__ XT thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
@@ -316,50 +338,54 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
         if (p >= pairs) continue;
         const int64_t g = r0 + r;
         float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-        int node = 0;
-        if (g < rows) node = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, w);
+        int packed = 0;
+        if (g < rows)
+            packed = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, sh.OT, H, w);
         W[static_cast<size_t>(p) * rows_pad + g] = w;
         const int64_t tile = g / sh.R;
         const int qc = static_cast<int>(g - tile * sh.R);
-        O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = node * sh.OT;
+        O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
     }
 }
 
 // K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
 // Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
-// [out_tile][pair][node][OT] fp32: the sheet of one (out_tile, pair) is one
-// contiguous (G+1)^2*OT*4-byte bulk copy and each node's OT outputs are a
+// [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of
+// it — is one contiguous bulk copy, and each node's OT outputs are a
 // contiguous, float4-aligned run.
 //
-// Pipeline (no CTA-wide barrier inside the pair loop):
-//   * sheets (+ records when staged): NBUF-deep ring in shared memory filled by
-//     the bulk-copy engine; "full[s]" mbarriers count the landed bytes. The LAST
-//     warp to finish with a slot (shared-memory atomic counter) issues the copy
-//     that refills it, so no warp waits on a producer and none is dedicated.
+// Pipeline over units u = (pair p, slab s), no CTA-wide barrier in the loop:
+//   * sheets (+ the pair's records when staged): NBUF-deep ring in shared memory
+//     filled by the bulk-copy engine; "full[slot]" mbarriers count landed bytes.
+//     The LAST warp to finish with a slot (shared-memory atomic counter) issues
+//     the copy that refills it, so no warp waits on a producer and none is
+//     dedicated to producing.
 //   * fused mode: every warp locates the cells of its own rows for the next pair
 //     into a warp-private record slice (x pair prefetched a pair ahead).
 //   * gather: lane group `sub` handles one row, lane c4 a float4 of outputs; per
 //     row one LDS.128 of weights and 4 LDS.128 of coefficients (nodes n, n+1,
-//     n+G+1, n+G+2), 16 FMAs; node offsets of a lane group's RT rows are
-//     contiguous (int4 loads).
+//     n+G+1, n+G+2), 16 FMAs; a lane group's RT node offsets are contiguous
+//     (int4 loads, kept in registers across the pair's slabs). With slabs
+//     (SLAB = true) a row is gathered only during its cell's slab.
 //
 // Accumulation order per (row, output): acc = 0; for p: acc += t_p with
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT, int MODE>
+template <int OT, int RT, typename XT, int MODE, bool SLAB>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
-                     const float* __restrict__ table, int pairs, int nbuf, float gamma,
+                     const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float4* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad) {
-    using S = FusedShape<OT, RT>;
-    constexpr int R = S::R;
+    using Sh = FusedShape<OT, RT>;
+    constexpr int R = Sh::R;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
-    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE);
+    const int H = (G + S - 1) / S;
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S);
     float* sheets = reinterpret_cast<float*>(smem);
     float4* rec_w = reinterpret_cast<float4*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
@@ -371,13 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int sub = lane / S::LPR, c4 = lane % S::LPR;
+    const int sub = lane / Sh::LPR, c4 = lane % Sh::LPR;
     const int64_t tile = blockIdx.x;
     const int64_t row0 = tile * R;
     const int ot = blockIdx.y;
     const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
     const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * OT;
+    const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * OT;  // slab stride within a sheet
     const int64_t tiles = rows_pad / R;
+    const int units = pairs * S;
 
     if constexpr (MODE != kModeStaged) {
         for (int k = tid; k < kMaxThr; k += kThreads) thr[k] = thr_of<XT>(gc)[k];
@@ -398,44 +426,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
 
-    auto issue = [&](int p) {  // one thread: sheet (+ records) of pair p into slot p % nbuf
-        const int s = p % nbuf;
-        const uint32_t rec_bytes = MODE == kModeStaged ? L.recw_bytes + L.reco_bytes : 0u;
-        mbar_arrive_expect_tx(&full[s], L.sheet_bytes + rec_bytes);
-        const char* src = reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * sheet_floats);
-        char* dst = reinterpret_cast<char*>(sheets) + static_cast<size_t>(s) * L.sheet_bytes;
+    auto issue = [&](int u) {  // one thread: slab (+ the pair's records when staged) of unit u
+        const int p = u / S, s = u - p * S;
+        const int slot = u % nbuf;
+        const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * OT * 4u;
+        const bool with_rec = MODE == kModeStaged && s == 0;
+        mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? L.recw_bytes + L.reco_bytes : 0u));
+        const char* src =
+            reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * sheet_floats + static_cast<size_t>(s) * slab_floats);
+        char* dst = reinterpret_cast<char*>(sheets) + static_cast<size_t>(slot) * L.sheet_bytes;
         constexpr uint32_t kChunk = 32768;
-        for (uint32_t o = 0; o < L.sheet_bytes; o += kChunk) {
-            const uint32_t n = L.sheet_bytes - o < kChunk ? L.sheet_bytes - o : kChunk;
-            bulk_g2s(dst + o, src + o, n, &full[s], policy);
+        for (uint32_t o = 0; o < bytes; o += kChunk) {
+            const uint32_t n = bytes - o < kChunk ? bytes - o : kChunk;
+            bulk_g2s(dst + o, src + o, n, &full[slot], policy);
         }
         if constexpr (MODE == kModeStaged) {
-            bulk_g2s(reinterpret_cast<char*>(rec_w) + s * L.recw_bytes,
-                     recW + static_cast<size_t>(p) * rows_pad + row0, L.recw_bytes, &full[s], policy_rec);
-            bulk_g2s(reinterpret_cast<char*>(rec_o) + s * L.reco_bytes,
-                     recO + (static_cast<size_t>(p) * tiles + tile) * S::OBLK, L.reco_bytes, &full[s], policy_rec);
+            if (with_rec) {
+                const int rs = p % L.nrec;
+                bulk_g2s(reinterpret_cast<char*>(rec_w) + rs * L.recw_bytes,
+                         recW + static_cast<size_t>(p) * rows_pad + row0, L.recw_bytes, &full[slot], policy_rec);
+                bulk_g2s(reinterpret_cast<char*>(rec_o) + rs * L.reco_bytes,
+                         recO + (static_cast<size_t>(p) * tiles + tile) * Sh::OBLK, L.reco_bytes, &full[slot],
+                         policy_rec);
+            }
         }
     };
     if constexpr (kSmemSheet) {
         if (tid == 0) {
-            const int pre = nbuf < pairs ? nbuf : pairs;
-            for (int p = 0; p < pre; ++p) issue(p);
+            const int pre = nbuf < units ? nbuf : units;
+            for (int u = 0; u < pre; ++u) issue(u);
         }
     }
 
     // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane
-    XT xa[S::LOC], xb[S::LOC];
-    const XT* xrow[S::LOC];
+    XT xa[Sh::LOC], xb[Sh::LOC];
+    const XT* xrow[Sh::LOC];
     const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0;
 #pragma unroll
-    for (int k = 0; k < S::LOC; ++k) {
+    for (int k = 0; k < Sh::LOC; ++k) {
         const int q = k * 32 + lane;
-        const int64_t r = row0 + warp * S::ROWS_W + q;
-        xrow[k] = (MODE != kModeStaged && q < S::ROWS_W && r < rows) ? X + r * n_in : nullptr;
+        const int64_t r = row0 + warp * Sh::ROWS_W + q;
+        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && r < rows) ? X + r * n_in : nullptr;
     }
     auto prefetch = [&](int p) {
 #pragma unroll
-        for (int k = 0; k < S::LOC; ++k) {
+        for (int k = 0; k < Sh::LOC; ++k) {
             if (xrow[k]) {
                 if (sizeof(XT) == 4 && x_vec_ok) {
                     const float2 v = __ldg(reinterpret_cast<const float2*>(xrow[k] + 2 * p));
@@ -451,17 +486,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
     auto locate = [&]() {
-        const ShapeRT sh = shape_rt(OT, RT);
+        const ShapeRT shp = shape_rt(OT, RT);
 #pragma unroll
-        for (int k = 0; k < S::LOC; ++k) {
+        for (int k = 0; k < Sh::LOC; ++k) {
             const int q = k * 32 + lane;
-            if (q < S::ROWS_W) {
+            if (q < Sh::ROWS_W) {
                 float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-                int node = 0;
-                if (xrow[k]) node = locate_record<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, w);
-                const int qc = warp * S::ROWS_W + q;
+                int packed = 0;
+                if (xrow[k]) packed = locate_record<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, OT, H, w);
+                const int qc = warp * Sh::ROWS_W + q;
                 rec_w[qc] = w;
-                rec_o[offset_slot(sh, qc)] = node * OT;
+                rec_o[offset_slot(shp, qc)] = packed;
             }
         }
     };
@@ -477,34 +512,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pairs > 1) prefetch(1);
         __syncwarp();
     }
-    for (int p = 0; p < pairs; ++p) {
+    int offs[RT];
+    const float4* rw = rec_w;
+    int p = 0, s = 0;
+    for (int u = 0; u < units; ++u) {
         const float* sh;
-        const float4* rw = rec_w + warp * S::ROWS_W + sub;
-        const int* ro = rec_o + (warp * S::RPW + sub) * S::OSTRIDE;
         if constexpr (kSmemSheet) {
-            const int s = p % nbuf;
-            mbar_wait(&full[s], static_cast<uint32_t>((p / nbuf) & 1));
-            sh = sheets + static_cast<size_t>(s) * sheet_floats + 4 * c4;
-            if constexpr (MODE == kModeStaged) {
-                rw += s * (L.recw_bytes / 16);
-                ro += s * (L.reco_bytes / 4);
-            }
+            const int slot = u % nbuf;
+            mbar_wait(&full[slot], static_cast<uint32_t>((u / nbuf) & 1));
+            sh = sheets + static_cast<size_t>(slot) * (L.sheet_bytes / 4) + 4 * c4;
         } else {
             sh = tsrc + static_cast<size_t>(p) * sheet_floats + 4 * c4;
         }
-        int offs[RT];
+        if (s == 0) {  // this pair's records: weights stay in smem, offsets go to registers
+            const int rs = MODE == kModeStaged ? p % L.nrec : 0;
+            rw = rec_w + rs * (L.recw_bytes / 16) + warp * Sh::ROWS_W + sub;
+            const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
 #pragma unroll
-        for (int k = 0; k < RT / 4; ++k) {
-            const int4 v = reinterpret_cast<const int4*>(ro)[k];
-            offs[4 * k] = v.x;
-            offs[4 * k + 1] = v.y;
-            offs[4 * k + 2] = v.z;
-            offs[4 * k + 3] = v.w;
+            for (int k = 0; k < RT / 4; ++k) {
+                const int4 v = reinterpret_cast<const int4*>(ro)[k];
+                offs[4 * k] = v.x;
+                offs[4 * k + 1] = v.y;
+                offs[4 * k + 2] = v.z;
+                offs[4 * k + 3] = v.w;
+            }
         }
 #pragma unroll
         for (int j = 0; j < RT; ++j) {
-            const float4 w = rw[j * S::RPW];
-            const float* b0 = sh + offs[j];
+            if constexpr (SLAB) {
+                if ((offs[j] >> kSlabShift) != s) continue;
+            }
+            const float4 w = rw[j * Sh::RPW];
+            const float* b0 = sh + (SLAB ? (offs[j] & kOffMask) : offs[j]);
             const float* b1 = b0 + rstride;
             float4 p00, p01, p10, p11;
             if constexpr (kSmemSheet) {
@@ -523,25 +562,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
             acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
         }
-        __syncwarp();  // this warp is done with its records and with sheet slot s
+        __syncwarp();  // this warp is done with slot u % nbuf (and, at s == S-1, with pair p's records)
         if constexpr (kSmemSheet) {
             if (lane == 0) {
-                const int s = p % nbuf;
+                const int slot = u % nbuf;
                 __threadfence_block();
-                if (atomicAdd(&cnt[s], 1u) == kWarps - 1) {  // last warp out refills the slot
-                    cnt[s] = 0;
-                    if (p + nbuf < pairs) {
+                if (atomicAdd(&cnt[slot], 1u) == kWarps - 1) {  // last warp out refills the slot
+                    cnt[slot] = 0;
+                    if (u + nbuf < units) {
                         fence_proxy_async();
-                        issue(p + nbuf);
+                        issue(u + nbuf);
                     }
                 }
             }
         }
-        if constexpr (MODE != kModeStaged) {
-            if (p + 1 < pairs) {
-                locate();
-                if (p + 2 < pairs) prefetch(p + 2);
-                __syncwarp();
+        if (++s == S) {
+            s = 0;
+            ++p;
+            if constexpr (MODE != kModeStaged) {
+                if (p < pairs) {
+                    locate();
+                    if (p + 1 < pairs) prefetch(p + 1);
+                    __syncwarp();
+                }
             }
         }
     }
@@ -551,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool y_vec_ok = (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (n_out & 3) == 0;
 #pragma unroll
     for (int j = 0; j < RT; ++j) {
-        const int64_t r = row0 + warp * S::ROWS_W + j * S::RPW + sub;
+        const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
         if (r >= rows) continue;
         const float v[4] = {acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma, acc[j].w * gamma};
         XT* yr = Y + r * n_out;
@@ -607,7 +650,7 @@ __device__ __forceinline__ float hash_normal(uint64_t seed, uint64_t f) {
     return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
 }
 
-__global__ void fill_random_kernel(float* __restrict__ dst, int pairs, int nodes, int n_out_total,
+static __global__ void fill_random_kernel(float* __restrict__ dst, int pairs, int nodes, int n_out_total,
                                    int out_begin, int n_out_local, int OT, int n_ot, uint64_t seed,
                                    float scale) {
     const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * OT;
@@ -630,7 +673,7 @@ __global__ void fill_random_kernel(float* __restrict__ dst, int pairs, int nodes
 }
 
 // Device table -> reference layout (doubles) for pairs [pb, pe), local outputs.
-__global__ void export_kernel(const float* __restrict__ table, double* __restrict__ dst, int pairs, int nodes,
+static __global__ void export_kernel(const float* __restrict__ table, double* __restrict__ dst, int pairs, int nodes,
                               int n_out_local, int OT, int pb, int pe) {
     const int np = pe - pb;
     const size_t total = static_cast<size_t>(nodes) * np * n_out_local;

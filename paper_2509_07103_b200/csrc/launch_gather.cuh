@@ -1,0 +1,56 @@
+// Gather-kernel launch templates (see layer_impl.hpp); included only by the
+// gather_ot*.cu translation units, each instantiating one output-tile width.
+#pragma once
+
+#include "layer_impl.hpp"
+
+namespace lmkan_b200 {
+
+template <int OT, int RT, typename XT, int MODE, bool SLAB>
+cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                           const float4* recW, const int* recO, cudaStream_t st) {
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB>;
+    static int configured[64] = {0};  // per device: dynamic-smem opt-in done
+    const int dev = L->device & 63;
+    if (!configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return e;
+        configured[dev] = 1;
+    }
+    dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
+    kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
+                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad);
+    return cudaGetLastError();
+}
+
+template <int OT, typename XT, int MODE, bool SLAB>
+cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                            const float4* recW, const int* recO, cudaStream_t st) {
+    switch (pl.RT) {
+        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
+        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
+        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
+    }
+}
+
+template <int OT, typename XT>
+cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                              const float4* recW, const int* recO, cudaStream_t st) {
+    if (pl.mode == kModeGlobal)
+        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, st);
+    if (pl.mode == kModeStaged)
+        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, st)
+                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, st);
+    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, st)
+                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, st);
+}
+
+}  // namespace lmkan_b200
+
+#define LMKAN_B200_INSTANTIATE_GATHER(OT)                                                                        \
+    template cudaError_t lmkan_b200::launch_gather<OT, float>(const lmkan_b200_layer*, const lmkan_b200::Plan&, \
+                                                              const float*, float*, int64_t, const float4*,      \
+                                                              const int*, cudaStream_t);                         \
+    template cudaError_t lmkan_b200::launch_gather<OT, double>(const lmkan_b200_layer*,                          \
+                                                               const lmkan_b200::Plan&, const double*, double*,  \
+                                                               int64_t, const float4*, const int*, cudaStream_t);

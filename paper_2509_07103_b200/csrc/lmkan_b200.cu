@@ -22,20 +22,9 @@
 #include "grid_host.hpp"
 #include "host_rng.hpp"
 #include "kernels.cuh"
+#include "layer_impl.hpp"
 
 using namespace lmkan_b200;
-
-struct lmkan_b200_layer {
-    int device = 0;
-    int n_in = 0, n_out = 0, G = 0, pairs = 0, nodes = 0;
-    int n_out_total = 0, out_begin = 0;
-    double gamma = 0.0;
-    int OT = 64, n_ot = 0;
-    float* table = nullptr;
-    size_t table_bytes = 0;
-    double* d_inv = nullptr;
-    GridConst gc{};
-};
 
 namespace {
 
@@ -97,34 +86,31 @@ int max_smem_optin(int device) {
 }
 
 // ---------------------------------------------------------------- planning
-struct Plan {
-    int OT, RT, nbuf, mode;
-    ShapeRT sh;
-    uint32_t smem;
-    int64_t row_tiles, rows_pad;
-    int launches;
-};
-
 constexpr int kRTChoices[] = {16, 8, 4};
 constexpr int kNumSMs = 148;
+constexpr int kMaxSlabs = 4;
 
 int rows_per_cta(int OT, int RT) { return shape_rt(OT, RT).R; }
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
 // Output tile width for a layer: the widest of {64, 32, 16} (not padding a
 // small layer by 2x or more) whose sheet can be double-buffered in shared
-// memory at some row tile; else the narrowest that fits single-buffered.
+// memory with at most kMaxSlabs i1-slabs; else the narrowest single-buffered.
 int choose_out_tile(int n_out, int G, int smem_cap) {
-    if (const char* e = std::getenv("LMKAN_B200_OT")) {
-        const int v = std::atoi(e);
-        if (v == 16 || v == 32 || v == 64 || v == 128) return v;
-    }
+    const int v = env_int("LMKAN_B200_OT", 0);
+    if (v == 16 || v == 32 || v == 64) return v;
     for (int want_buf : {2, 1}) {
         for (int OT : {64, 32, 16}) {
             if (OT > 16 && OT / 2 >= n_out) continue;
-            for (int RT : kRTChoices) {
-                const FusedSmem s = fused_smem_layout(G, OT, RT, want_buf, kModeStaged);
-                if (static_cast<int>(s.total) <= smem_cap) return OT;
-            }
+            for (int S = 1; S <= (want_buf == 2 ? 3 : 1); ++S)
+                for (int RT : kRTChoices) {
+                    const FusedSmem s = fused_smem_layout(G, OT, RT, want_buf, kModeStaged, S);
+                    if (static_cast<int>(s.total) <= smem_cap) return OT;
+                }
         }
     }
     return 16;
@@ -133,11 +119,13 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
 // Mode: staged (K1 + K2) when several output tiles re-read the same cells (the
 // locate then runs once per (row, pair) instead of once per output tile and
 // the gather kernel's shared-memory port serves only gathers); fused (K3)
-// otherwise; global-sheet fallback when no sheet fits shared memory.
+// otherwise; global-sheet fallback when nothing fits shared memory.
+// Within a mode: prefer double buffering with the fewest slabs, then the
+// largest row tile that still fills the GPU with one wave of CTAs.
 bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
-    int force_rt = 0, force_nbuf = 0, force_mode = -1;
-    if (const char* e = std::getenv("LMKAN_B200_RT")) force_rt = std::atoi(e);
-    if (const char* e = std::getenv("LMKAN_B200_NBUF")) force_nbuf = std::atoi(e);
+    const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
+              force_s = env_int("LMKAN_B200_SLABS", 0);
+    int force_mode = -1;
     if (const char* e = std::getenv("LMKAN_B200_MODE")) {
         if (!std::strcmp(e, "fused")) force_mode = kModeFused;
         if (!std::strcmp(e, "staged")) force_mode = kModeStaged;
@@ -147,58 +135,32 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
     for (int mode : modes) {
         if (force_mode >= 0 && mode != force_mode) continue;
-        for (int RT : kRTChoices) {
-            if (force_rt && RT != force_rt) continue;
-            const ShapeRT sh = shape_rt(L->OT, RT);
-            const int64_t tiles = (rows + sh.R - 1) / sh.R;
-            // prefer the largest row tile that still gives >= one wave of CTAs
-            if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
-            const bool smem_sheet = mode != kModeGlobal;
-            for (int nbuf = smem_sheet ? 4 : 0; nbuf >= (smem_sheet ? 1 : 0); --nbuf) {
-                if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
-                if (smem_sheet && nbuf > L->pairs && nbuf > 1) continue;
-                const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode);
-                if (static_cast<int>(s.total) > smem_cap) continue;
-                out = Plan{L->OT, RT, nbuf, mode, sh, s.total, tiles, tiles * sh.R, mode == kModeStaged ? 2 : 1};
-                return true;
+        const bool smem_sheet = mode != kModeGlobal;
+        for (int min_buf : {2, 1}) {
+            if (!smem_sheet && min_buf == 2) continue;
+            for (int S = 1; S <= (smem_sheet ? kMaxSlabs : 1); ++S) {
+                if (force_s && S != force_s) continue;
+                if (S > 1 && min_buf == 1) continue;
+                for (int RT : kRTChoices) {
+                    if (force_rt && RT != force_rt) continue;
+                    const ShapeRT sh = shape_rt(L->OT, RT);
+                    const int64_t tiles = (rows + sh.R - 1) / sh.R;
+                    if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
+                    for (int nbuf = smem_sheet ? 4 : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
+                        if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
+                        const int units = L->pairs * S;
+                        if (smem_sheet && nbuf > units && nbuf > 1) continue;
+                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S);
+                        if (static_cast<int>(s.total) > smem_cap) continue;
+                        out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, tiles, tiles * sh.R,
+                                   mode == kModeStaged ? 2 : 1};
+                        return true;
+                    }
+                }
             }
         }
     }
     return false;
-}
-
-template <int OT, int RT, typename XT, int MODE>
-cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                           const float4* recW, const int* recO, cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT, MODE>;
-    static int configured[64] = {0};  // per device: dynamic-smem opt-in done
-    const int dev = L->device & 63;
-    if (!configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        if (e != cudaSuccess) return e;
-        configured[dev] = 1;
-    }
-    dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
-    kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf,
-                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad);
-    return cudaGetLastError();
-}
-
-template <int OT, typename XT>
-cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                            const float4* recW, const int* recO, cudaStream_t st) {
-    if (pl.mode == kModeGlobal) return launch_fused_t<OT, 4, XT, kModeGlobal>(L, pl, X, Y, rows, recW, recO, st);
-#define LMKAN_RT_CASES(MODE)                                                                        \
-    switch (pl.RT) {                                                                                \
-        case 16: return launch_fused_t<OT, 16, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);        \
-        case 8: return launch_fused_t<OT, 8, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);          \
-        default: return launch_fused_t<OT, 4, XT, MODE>(L, pl, X, Y, rows, recW, recO, st);         \
-    }
-    if (pl.mode == kModeStaged) {
-        LMKAN_RT_CASES(kModeStaged)
-    }
-    LMKAN_RT_CASES(kModeFused)
-#undef LMKAN_RT_CASES
 }
 
 template <typename XT>
@@ -228,8 +190,9 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
         dim3 g1(static_cast<unsigned>(pl.rows_pad / 64), static_cast<unsigned>((L->pairs + 15) / 16));
+        const int H = (L->G + pl.S - 1) / pl.S;
         records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
-                                                                            pl.sh, recW, recO);
+                                                                            pl.sh, H, recW, recO);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(recW, st);
@@ -240,10 +203,9 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
     switch (L->OT) {
-        case 128: e = launch_fused_rt<128, XT>(L, pl, X, Y, rows, recW, recO, st); break;
-        case 64: e = launch_fused_rt<64, XT>(L, pl, X, Y, rows, recW, recO, st); break;
-        case 32: e = launch_fused_rt<32, XT>(L, pl, X, Y, rows, recW, recO, st); break;
-        default: e = launch_fused_rt<16, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, recW, recO, st); break;
     }
     if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
@@ -576,7 +538,7 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i
 }
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
-                    int* rows_per_cta_out, int* launches, int* mode) {
+                    int* rows_per_cta_out, int* launches, int* mode, int* slabs) {
     if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits");
@@ -586,6 +548,7 @@ int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int*
     if (rows_per_cta_out) *rows_per_cta_out = pl.sh.R;
     if (launches) *launches = pl.launches;
     if (mode) *mode = pl.mode;
+    if (slabs) *slabs = pl.S;
     return LMKAN_B200_OK;
 }
 

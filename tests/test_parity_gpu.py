@@ -236,3 +236,40 @@ def test_f64_device_path(torch, pkg, oracle):
     Y = layer.forward(torch.from_numpy(X).cuda()).cpu().numpy()
     ref = oracle.forward(G, layer.read_table(), X, 1.0)
     assert _mixed(Y, ref).max() <= TOL
+
+
+VARIANTS = [("fused", "1", "16"), ("fused", "2", "8"), ("fused", "3", "4"), ("staged", "1", "16"),
+            ("staged", "2", "16"), ("staged", "3", "8"), ("staged", "4", "4"), ("global", "1", "4")]
+
+
+@pytest.mark.parametrize("G", [8, 28, 32])
+def test_kernel_variants_parity_and_bitwise_agreement(torch, pkg, oracle, monkeypatch, G):
+    """Every kernel variant (fused / staged / global-sheet, 1-4 i1-slabs, row
+    tiles) meets the parity bar AND agrees bitwise with every other variant:
+    the per-(row, output) summation order does not depend on the variant."""
+    n_in, n_out, rows = 40, 72, 1300
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=G + 100, xscale=1.3)
+    Xd = torch.from_numpy(X).cuda()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 1.0)
+    outs = []
+    for ot in ("16", "32", "64"):
+        monkeypatch.setenv("LMKAN_B200_OT", ot)
+        layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+        for mode, slabs, rt in VARIANTS:
+            monkeypatch.setenv("LMKAN_B200_MODE", mode)
+            monkeypatch.setenv("LMKAN_B200_SLABS", slabs)
+            monkeypatch.setenv("LMKAN_B200_RT", rt)
+            try:
+                plan = layer.plan(rows)
+            except ValueError:
+                continue  # this variant does not fit shared memory at this G / OT
+            assert plan["mode"] == mode and str(plan["slabs"]) == slabs and str(plan["rows_per_thread"]) == rt
+            Y = layer.forward(Xd)
+            assert _mixed(Y.cpu().numpy(), ref).max() <= TOL, (ot, mode, slabs, rt)
+            outs.append(((ot, mode, slabs, rt), Y))
+        for k in ("LMKAN_B200_MODE", "LMKAN_B200_SLABS", "LMKAN_B200_RT"):
+            monkeypatch.delenv(k)
+    assert len(outs) >= 8
+    base = outs[0][1]
+    for name, Y in outs[1:]:
+        assert torch.equal(Y, base), name
