@@ -70,6 +70,21 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// Predicated 128-bit shared-memory load: zeros (and no shared-memory traffic)
+// when !pred. Keeps the slab-mode gather loop branch-free.
+__device__ __forceinline__ float4 lds128_if(const void* p, bool pred) {
+    float4 v;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "mov.f32 %0, 0f00000000;\n\tmov.f32 %1, 0f00000000;\n\t"
+        "mov.f32 %2, 0f00000000;\n\tmov.f32 %3, 0f00000000;\n\t"
+        "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(smem_addr(p)), "r"(static_cast<int>(pred))
+        : "memory");
+    return v;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -524,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             sh = tsrc + static_cast<size_t>(p) * sheet_floats + 4 * c4;
         }
-        if (s == 0) {  // this pair's records: weights stay in smem, offsets go to registers
+        if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets to registers (kept across slabs)
             const int rs = MODE == kModeStaged ? p % L.nrec : 0;
             rw = rec_w + rs * (L.recw_bytes / 16) + warp * Sh::ROWS_W + sub;
             const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
@@ -539,23 +554,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int j = 0; j < RT; ++j) {
+            float4 w, p00, p01, p10, p11;
             if constexpr (SLAB) {
-                if ((offs[j] >> kSlabShift) != s) continue;
-            }
-            const float4 w = rw[j * Sh::RPW];
-            const float* b0 = sh + (SLAB ? (offs[j] & kOffMask) : offs[j]);
-            const float* b1 = b0 + rstride;
-            float4 p00, p01, p10, p11;
-            if constexpr (kSmemSheet) {
-                p00 = *reinterpret_cast<const float4*>(b0);
-                p01 = *reinterpret_cast<const float4*>(b0 + OT);
-                p10 = *reinterpret_cast<const float4*>(b1);
-                p11 = *reinterpret_cast<const float4*>(b1 + OT);
+                // rows whose cell lies in another slab load nothing and add +0
+                const bool v = (offs[j] >> kSlabShift) == s;
+                const float* b0 = sh + (offs[j] & kOffMask);
+                const float* b1 = b0 + rstride;
+                w = lds128_if(rw + j * Sh::RPW, v);
+                p00 = lds128_if(b0, v);
+                p01 = lds128_if(b0 + OT, v);
+                p10 = lds128_if(b1, v);
+                p11 = lds128_if(b1 + OT, v);
             } else {
-                p00 = __ldg(reinterpret_cast<const float4*>(b0));
-                p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
-                p10 = __ldg(reinterpret_cast<const float4*>(b1));
-                p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+                w = rw[j * Sh::RPW];
+                const float* b0 = sh + offs[j];
+                const float* b1 = b0 + rstride;
+                if constexpr (kSmemSheet) {
+                    p00 = *reinterpret_cast<const float4*>(b0);
+                    p01 = *reinterpret_cast<const float4*>(b0 + OT);
+                    p10 = *reinterpret_cast<const float4*>(b1);
+                    p11 = *reinterpret_cast<const float4*>(b1 + OT);
+                } else {
+                    p00 = __ldg(reinterpret_cast<const float4*>(b0));
+                    p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
+                    p10 = __ldg(reinterpret_cast<const float4*>(b1));
+                    p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+                }
             }
             acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
             acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));

@@ -14,7 +14,7 @@ tail -c 1500 gpurun_out/${TAG}_bench.json
 if [ "${NCU:-1}" = 1 ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
      --log-file gpurun_out/${TAG}_launches.csv python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_fused -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_fused -s ${NCU_SKIP:-3} -c 1 \
      -o gpurun_out/${TAG}_prof -f python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu.log 2>&1
   tail -3 gpurun_out/${TAG}_ncu.log
 fi
