@@ -209,7 +209,7 @@ class Layer:
         check(lib.lmkan_b200_plan(self._h, int(rows), *[C.byref(x) for x in v]))
         d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode", "slabs"],
                      [x.value for x in v]))
-        d["mode"] = {0: "fused", 1: "staged", 2: "global"}[d["mode"]]
+        d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow"}[d["mode"]]
         return d
 
     def close(self) -> None:

@@ -228,6 +228,7 @@ enum : int {
     kModeFused = 0,   // K3: cells located in-kernel (warp-local), sheets via bulk copy
     kModeStaged = 1,  // K2: cell records produced by K1 (records_kernel), sheets + records via bulk copy
     kModeGlobal = 2,  // fallback for sheets larger than shared memory: in-kernel locate, sheets read from L2
+    kModeNarrow = 3,  // K4: n_out <= 4, whole table resident in shared memory, lanes over pairs
 };
 
 // Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
@@ -631,6 +632,82 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
             if (col + e < n_out) yr[col + e] = static_cast<XT>(v[e]);
+    }
+}
+
+// K4: narrow layers (n_out <= 4, e.g. the methane net's 128 -> 1 head). A
+// padded 16-wide output tile would waste >= 3/4 of every gather, so instead the
+// whole table, laid out [pair][node][NO] (NO = n_out rounded up to 1, 2 or 4),
+// is made resident in shared memory once per CTA (bulk copy), a warp walks
+// rows, each lane takes pairs p = lane, lane + 32, ... (row-contiguous x-pair
+// loads), locates, gathers its 4 corners and keeps a partial sum; a shuffle
+// tree reduces the 32 partials. Summation order: per lane over its pairs in
+// increasing p, then the fixed xor tree — deterministic, not the reference's
+// single chain (within the 1e-5 contract).
+__host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) {
+    const uint32_t tab = static_cast<uint32_t>((G + 1) * (G + 1)) * pairs * NO * 4u;
+    uint32_t o = (tab + 15u) & ~15u;
+    o += kMaxThr * 8u + (kMaxThr + 1) * 8u + static_cast<uint32_t>(G) * G * 8u + 16u;
+    return (o + 127u) & ~127u;
+}
+
+template <typename XT, int NO>
+__global__ void __launch_bounds__(256) narrow_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows,
+                                                     int n_in, int n_out, const float* __restrict__ table, float gamma,
+                                                     const __grid_constant__ GridConst gc) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int G = gc.G, pairs = n_in / 2, nodes = (G + 1) * (G + 1);
+    const uint32_t tab_bytes = static_cast<uint32_t>(nodes) * pairs * NO * 4u;
+    float* tab = reinterpret_cast<float*>(smem);
+    uint32_t o = (tab_bytes + 15u) & ~15u;
+    XT* thr = reinterpret_cast<XT*>(smem + o);
+    o += kMaxThr * 8u;
+    double* pts = reinterpret_cast<double*>(smem + o);
+    o += (kMaxThr + 1) * 8u;
+    double* inv = reinterpret_cast<double*>(smem + o);
+    o += static_cast<uint32_t>(G) * G * 8u;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((o + 7u) & ~7u));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
+    for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(bar, tab_bytes);
+        const uint64_t pol = policy_evict_last();
+        constexpr uint32_t kChunk = 32768;
+        for (uint32_t c = 0; c < tab_bytes; c += kChunk)
+            bulk_g2s(smem + c, reinterpret_cast<const char*>(table) + c, tab_bytes - c < kChunk ? tab_bytes - c : kChunk,
+                     bar, pol);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    const int rs1 = (G + 1) * NO;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + warp; r < rows; r += static_cast<int64_t>(gridDim.x) * 8) {
+        float part[NO];
+#pragma unroll
+        for (int q = 0; q < NO; ++q) part[q] = 0.f;
+        const XT* xr = X + r * n_in;
+        for (int p = lane; p < pairs; p += 32) {
+            float4 w;
+            const int off = locate_record<XT>(xr[2 * p], xr[2 * p + 1], thr, pts, inv, G, gc.L, NO, G, w);
+            const float* b = tab + static_cast<size_t>(p) * nodes * NO + off;
+#pragma unroll
+            for (int q = 0; q < NO; ++q)
+                part[q] += fmaf(w.w, b[rs1 + NO + q], fmaf(w.z, b[NO + q], fmaf(w.y, b[rs1 + q], w.x * b[q])));
+        }
+#pragma unroll
+        for (int q = 0; q < NO; ++q)
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], m);
+        if (lane < n_out) {
+            float v = part[0];
+#pragma unroll
+            for (int q = 1; q < NO; ++q)
+                if (lane == q) v = part[q];
+            Y[r * n_out + lane] = static_cast<XT>(v * gamma);
+        }
     }
 }
 

@@ -13,6 +13,7 @@ struct lmkan_b200_layer {
     int n_out_total = 0, out_begin = 0;
     double gamma = 0.0;
     int OT = 64, n_ot = 0;
+    bool narrow = false;  // n_out <= 4: [pair][node][OT] table, K4 narrow kernel
     float* table = nullptr;
     size_t table_bytes = 0;
     double* d_inv = nullptr;

@@ -103,6 +103,9 @@ int env_int(const char* name, int dflt) {
 int choose_out_tile(int n_out, int G, int smem_cap) {
     const int v = env_int("LMKAN_B200_OT", 0);
     if (v == 16 || v == 32 || v == 64) return v;
+    // Large grids: the (G+1)^2-node sheet streamed per pair dominates, so the
+    // tallest row tile (OT = 16 -> 2048 rows per CTA) wins (measured at G = 28).
+    if (G >= 24) return 16;
     for (int want_buf : {2, 1}) {
         for (int OT : {64, 32, 16}) {
             if (OT > 16 && OT / 2 >= n_out) continue;
@@ -125,6 +128,12 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
 bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
               force_s = env_int("LMKAN_B200_SLABS", 0);
+    if (L->narrow) {
+        const int64_t ctas = std::min<int64_t>(kNumSMs, (rows + 7) / 8);
+        out = Plan{L->OT, 1, 1, kModeNarrow, 1, shape_rt(16, 4), narrow_smem_bytes(L->G, L->pairs, L->OT), ctas,
+                   rows, 1};
+        return static_cast<int>(out.smem) <= smem_cap;
+    }
     int force_mode = -1;
     if (const char* e = std::getenv("LMKAN_B200_MODE")) {
         if (!std::strcmp(e, "fused")) force_mode = kModeFused;
@@ -163,20 +172,38 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     return false;
 }
 
+// Cap on the stream-ordered cell-record scratch of the staged mode; larger
+// batches are processed in row chunks (LMKAN_B200_MAX_SCRATCH_MB overrides).
+size_t record_scratch_cap() { return static_cast<size_t>(env_int("LMKAN_B200_MAX_SCRATCH_MB", 4096)) << 20; }
+
+// One launch group (K1 + K2 in staged mode, K3 otherwise) over `rows` rows.
+template <typename XT, int NO>
+cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+                          cudaStream_t st) {
+    static int configured[64] = {0};
+    if (!configured[L->device & 63]) {
+        cudaError_t e =
+            cudaFuncSetAttribute(narrow_kernel<XT, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return e;
+        configured[L->device & 63] = 1;
+    }
+    narrow_kernel<XT, NO><<<static_cast<unsigned>(pl.row_tiles), 256, pl.smem, st>>>(
+        X, Y, rows, L->n_in, L->n_out, L->table, static_cast<float>(L->gamma), L->gc);
+    return cudaGetLastError();
+}
+
 template <typename XT>
-int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
-                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr) {
-    if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
-    if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
-    if (rows == 0) return LMKAN_B200_OK;
-    if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
-    if (reinterpret_cast<uintptr_t>(Y) % sizeof(XT) != 0 || reinterpret_cast<uintptr_t>(X) % sizeof(XT) != 0)
-        return fail(LMKAN_B200_EINVAL, "lmkan_forward: X and Y must be aligned to their element size");
-    DeviceGuard g(L->device);
-    Plan pl;
-    if (!make_plan(L, rows, max_smem_optin(L->device), pl))
-        return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory (G too large)");
-    if (pl.row_tiles > 0x7fffffff) return fail(LMKAN_B200_EINVAL, "lmkan_forward: batch too large");
+int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
+                 cudaEvent_t ev_begin, cudaEvent_t ev_end) {
+    if (pl.mode == kModeNarrow) {
+        if (ev_begin) cudaEventRecord(ev_begin, st);
+        const cudaError_t e = L->OT == 1   ? launch_narrow<XT, 1>(L, pl, X, Y, rows, st)
+                              : L->OT == 2 ? launch_narrow<XT, 2>(L, pl, X, Y, rows, st)
+                                           : launch_narrow<XT, 4>(L, pl, X, Y, rows, st);
+        if (ev_end) cudaEventRecord(ev_end, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: narrow kernel launch");
+        return LMKAN_B200_OK;
+    }
     float4* recW = nullptr;
     int* recO = nullptr;
     if (pl.mode == kModeStaged) {
@@ -211,6 +238,41 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
     if (recW) cudaFreeAsync(recW, st);
     if (recO) cudaFreeAsync(recO, st);
     if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: gather kernel launch");
+    return LMKAN_B200_OK;
+}
+
+template <typename XT>
+int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
+                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
+    if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
+    if (rows == 0) return LMKAN_B200_OK;
+    if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
+    if (reinterpret_cast<uintptr_t>(Y) % sizeof(XT) != 0 || reinterpret_cast<uintptr_t>(X) % sizeof(XT) != 0)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: X and Y must be aligned to their element size");
+    DeviceGuard g(L->device);
+    const int cap = max_smem_optin(L->device);
+    Plan pl;
+    if (!make_plan(L, rows, cap, pl))
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory (G too large)");
+    int64_t chunk = rows;
+    if (pl.mode == kModeStaged) {
+        const size_t per_row = static_cast<size_t>(L->pairs) * (sizeof(float4) + sizeof(int) * 2);
+        const int64_t max_rows = static_cast<int64_t>(record_scratch_cap() / per_row) / pl.sh.R * pl.sh.R;
+        if (rows > max_rows) chunk = std::max<int64_t>(max_rows, pl.sh.R);
+    }
+    if ((chunk + pl.sh.R - 1) / pl.sh.R > 0x7fffffff)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: batch too large");
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+        const int64_t n = std::min(chunk, rows - r0);
+        Plan pc = pl;
+        if (n != rows && !make_plan(L, n, cap, pc))
+            return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
+        const bool first = r0 == 0, last = r0 + n >= rows;
+        if (int rc = forward_rows<XT>(L, pc, X + r0 * L->n_in, Y + r0 * L->n_out, n, st, first ? ev_begin : nullptr,
+                                      last ? ev_end : nullptr))
+            return rc;
+    }
     return LMKAN_B200_OK;
 }
 
@@ -258,7 +320,14 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     L->pairs = n_in / 2;
     L->nodes = (G + 1) * (G + 1);
     L->gamma = gamma;
-    L->OT = choose_out_tile(n_out_local, G, max_smem_optin(device));
+    const int no = n_out_local <= 1 ? 1 : (n_out_local <= 2 ? 2 : 4);
+    if (n_out_local <= 4 && env_int("LMKAN_B200_NARROW", 1) &&
+        static_cast<int>(narrow_smem_bytes(G, n_in / 2, no)) <= max_smem_optin(device)) {
+        L->narrow = true;
+        L->OT = no;
+    } else {
+        L->OT = choose_out_tile(n_out_local, G, max_smem_optin(device));
+    }
     L->n_ot = (n_out_local + L->OT - 1) / L->OT;
     std::vector<double> pts, inv, t64;
     std::vector<float> t32;

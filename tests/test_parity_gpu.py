@@ -273,3 +273,49 @@ def test_kernel_variants_parity_and_bitwise_agreement(torch, pkg, oracle, monkey
     base = outs[0][1]
     for name, Y in outs[1:]:
         assert torch.equal(Y, base), name
+
+
+def test_staged_row_chunking_bitwise(torch, pkg, monkeypatch):
+    """Batches whose cell-record scratch exceeds the cap run in row chunks;
+    results are bitwise identical to the unchunked launch."""
+    n_in, n_out, G, rows = 256, 256, 16, 9000
+    layer = pkg.Layer.random(n_in, n_out, G, seed=8)
+    X = torch.randn((rows, n_in), device="cuda")
+    monkeypatch.setenv("LMKAN_B200_MODE", "staged")
+    Y1 = layer.forward(X)
+    monkeypatch.setenv("LMKAN_B200_MAX_SCRATCH_MB", "2")  # 2 MB -> ~ 1.6k-row chunks
+    Y2 = layer.forward(X)
+    assert torch.equal(Y1, Y2)
+
+
+def test_cfg5_shape_output_slice(torch, pkg, oracle):
+    """Config-5 geometry (8192 -> 8192, G = 32, 4096 pairs per output): an
+    output-sharded slice of the device-generated table, checked against the
+    oracle on a row subset (the longest accumulation chain of any config)."""
+    n_in, n_out, G, rows = 8192, 8192, 32, 48
+    ob, oe = 4096, 4112
+    layer = pkg.Layer.random(n_in, n_out, G, seed=55, out_range=(ob, oe))
+    P = layer.read_table()
+    X = torch.randn((rows, n_in), generator=torch.Generator().manual_seed(5)).float()
+    Y = layer.forward(X.cuda()).cpu().numpy()
+    ref = oracle.forward(G, P, X.double().numpy(), 1.0)
+    assert _mixed(Y, ref).max() <= TOL
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows", [(128, 1, 28, 3000), (64, 2, 16, 2000), (30, 3, 8, 999),
+                                               (2, 4, 5, 100), (200, 1, 12, 513)])
+def test_narrow_kernel(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows):
+    """n_out <= 4 layers run the narrow kernel (whole table in shared memory,
+    lanes over pairs); parity vs the oracle and vs the padded general path."""
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in + 7 * n_out)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 0.9)
+    assert layer.plan(rows)["mode"] == "narrow"
+    Xd = torch.from_numpy(X).cuda()
+    Y = layer.forward(Xd).cpu().numpy()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 0.9)
+    assert _mixed(Y, ref).max() <= TOL
+    assert np.array_equal(layer.forward(Xd).cpu().numpy(), Y)  # deterministic
+    monkeypatch.setenv("LMKAN_B200_NARROW", "0")
+    wide = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 0.9)
+    assert wide.plan(rows)["mode"] != "narrow"
+    assert _mixed(wide.forward(Xd).cpu().numpy(), ref).max() <= TOL
