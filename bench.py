@@ -37,8 +37,8 @@ CONFIGS = {
     2: dict(name="cfg2: lmKAN layer 1024->1024, G=16, batch 65536", layers=[(1024, 1024)], G=16, batch=65536),
     3: dict(name="cfg3: methane pure-lookup chain 12->128->128->1, G=28, batch 1048576",
             layers=[(12, 128), (128, 128), (128, 1)], G=28, batch=1 << 20),
-    4: dict(name="cfg4: 3x3 conv im2col rows, 144->16, G=16, 256 images x 1024 rows", layers=[(144, 16)],
-            G=16, batch=262144),
+    4: dict(name="cfg4: lmKAN 3x3 conv (implicit im2col), 144->16, G=16, 256 images 32x32x16 (zero-padded 34x34)",
+            layers=[(144, 16)], G=16, batch=262144, conv=dict(N=256, H=34, W=34, C=16, k=3, s=1)),
 }
 METRIC = "lmKAN layer fwd samples/s at 1/2/4/8 B200; achieved GB/s vs HBM roofline"
 
@@ -244,7 +244,16 @@ def main():
     layers = [pkg.Layer.random(n_in, n_out, G, seed=1000 + i, gamma=1.0, device=local)
               for i, (n_in, n_out) in enumerate(cfg["layers"])]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + rank)
-    X = torch.randn((B, cfg["layers"][0][0]), generator=gen, device=f"cuda:{local}", dtype=torch.float32)
+    conv = cfg.get("conv")
+    if conv:  # NHWC image batch; patch rows are formed on the fly (implicit im2col)
+        X = torch.randn((conv["N"], conv["H"], conv["W"], conv["C"]), generator=gen, device=f"cuda:{local}",
+                        dtype=torch.float32)
+        X[:, 0] = 0
+        X[:, -1] = 0
+        X[:, :, 0] = 0
+        X[:, :, -1] = 0  # zero padding ring of the 32x32 images
+    else:
+        X = torch.randn((B, cfg["layers"][0][0]), generator=gen, device=f"cuda:{local}", dtype=torch.float32)
     acts = [torch.empty((B, n_out), device=f"cuda:{local}", dtype=torch.float32) for _, n_out in cfg["layers"]]
     stream = torch.cuda.current_stream()
     K = args.steps
@@ -257,10 +266,18 @@ def main():
             a.record(stream)
             b.record(stream)
 
-    def step(i=None):
-        cur = X
+    def step(i=None, src=None):
+        cur = X if src is None else src
         for li, (lay, out) in enumerate(zip(layers, acts)):
-            if i is None:
+            if conv and li == 0:
+                if i is not None:
+                    gev[i][li][0].record(stream)
+                lay.conv_forward(cur, conv["k"], conv["s"], Y=out.view(conv["N"], (conv["H"] - conv["k"]) // conv["s"] + 1,
+                                                       (conv["W"] - conv["k"]) // conv["s"] + 1, -1),
+                                 stream=stream)
+                if i is not None:
+                    gev[i][li][1].record(stream)
+            elif i is None:
                 lay.forward_into(cur, out, stream)
             else:
                 lay.forward_into_timed(cur, out, gev[i][li][0], gev[i][li][1], stream)
@@ -296,18 +313,28 @@ def main():
     kernel_ms = statistics.mean(gather_ms)  # gather kernel(s) of one step, event-timed on the launch stream
     launches_per_step = sum(l.plan(B)["launches"] for l in layers)
 
-    # ---- e2e through the public host entry point (pinned host X in, host Y out)
+    # ---- e2e through the public API: pinned host input in, host result out.
+    # Single dense layer: the synchronous host entry lmkan_b200_forward_host_f32
+    # (H2D / kernels / D2H pipelined over row chunks inside the library).
+    # Chains and conv: H2D of the input, the device chain, D2H of the final
+    # output, on the bench stream (no overlap), then a host read of the result.
     e2e = None
     if not args.no_e2e:
         Xh = X.cpu().pin_memory()
-        Yh = [torch.empty((B, n_out), dtype=torch.float32).pin_memory() for _, n_out in cfg["layers"]]
+        n_last = cfg["layers"][-1][1]
+        Yh = torch.empty((B, n_last), dtype=torch.float32).pin_memory()
+        single = len(layers) == 1 and not conv
 
         def host_step():
-            cur = Xh
-            for lay, out in zip(layers, Yh):
-                lay.forward_host_ptr(cur.data_ptr(), out.data_ptr(), B, np.float32)
-                cur = out
-            return float(Yh[-1][0, 0])  # the step's result read on the host
+            if single:
+                layers[0].forward_host_ptr(Xh.data_ptr(), Yh.data_ptr(), B, np.float32)
+            else:
+                Xd = torch.empty_like(X)
+                Xd.copy_(Xh, non_blocking=True)
+                step(src=Xd)
+                Yh.copy_(acts[-1], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            return float(Yh[0, 0])  # the step's result read on the host
 
         for _ in range(2):
             host_step()
@@ -322,10 +349,11 @@ def main():
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         dt = float(te.item())
-        h2d = B * sum(n_in for n_in, _ in cfg["layers"]) * 4
-        d2h = B * sum(n_out for _, n_out in cfg["layers"]) * 4
+        h2d = X.numel() * 4
+        d2h = B * n_last * 4
         e2e = {"value": ws * B / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": dt * 1e3, "timer": "host wall clock around the synchronous host-path call"}
+               "ms_per_step": dt * 1e3,
+               "timer": "host wall clock around H2D + forward + D2H + host read (public API)"}
 
     if rank != 0:
         if dist:

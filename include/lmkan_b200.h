@@ -120,6 +120,16 @@ int lmkan_b200_forward_f32_timed(const lmkan_b200_layer* layer, const float* X_d
  * the fp64 thresholds, so indices stay bit-exact for any double X). */
 int lmkan_b200_forward_f64(const lmkan_b200_layer* layer, const double* X_dev, double* Y_dev,
                            int64_t rows, void* stream);
+/* Implicit-im2col convolution (the caller-side chain unfold_conv ->
+ * lmkan_forward -> fold_output, conv.hpp:39-71 + layer.hpp:108-134, in one
+ * device call): img_dev is an NHWC fp32 batch [N][H][W][C], taps k x k with
+ * stride s, and the layer's n_in must equal k*k*C (columns ordered
+ * (dy*k + dx)*C + ch as in unfold_conv). Patch rows are formed on the fly from
+ * the image (no patch matrix); Y_dev is [N][out_h][out_w][n_out] NHWC, i.e.
+ * fold_output's layout, out_h = (H-k)/s + 1. Same EINVAL conditions and
+ * messages as unfold_conv. */
+int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* layer, const float* img_dev, int N, int H,
+                                int W, int C, int k, int s, float* Y_dev, void* stream);
 /* Drop-in synchronous host paths: X/Y in host memory (pinned or pageable),
  * copies and kernels pipelined over row chunks on internal streams; returns
  * when Y is on the host. `workers` is accepted for signature parity with

@@ -156,6 +156,20 @@ class Layer:
         check(lib.lmkan_b200_forward_f32_timed(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream),
                                                C.c_void_p(ev_begin.cuda_event), C.c_void_p(ev_end.cuda_event)))
 
+    def conv_forward(self, img, k: int, s: int = 1, Y=None, stream=None):
+        """Implicit-im2col conv: img [N, H, W, C] float32 CUDA tensor (NHWC) ->
+        Y [N, out_h, out_w, n_out] (unfold_conv -> lmkan_forward -> fold_output,
+        conv.hpp:39-71, without materializing the patch matrix)."""
+        import torch
+        assert img.dtype == torch.float32 and img.is_cuda and img.is_contiguous() and img.dim() == 4
+        N, H, W, Cc = img.shape
+        oh, ow = (H - k) // s + 1, (W - k) // s + 1
+        if Y is None:
+            Y = torch.empty((N, max(oh, 0), max(ow, 0), self.n_out), dtype=torch.float32, device=img.device)
+        check(lib.lmkan_b200_conv_forward_f32(self._h, _ptr(img), int(N), int(H), int(W), int(Cc), int(k), int(s),
+                                              _ptr(Y), _stream_ptr(stream)))
+        return Y
+
     def forward(self, X, stream=None):
         """torch CUDA tensor in -> CUDA tensor out; numpy in -> numpy out (host path)."""
         if isinstance(X, np.ndarray):

@@ -39,6 +39,32 @@ struct GridConst {
     int L;  // power of two >= G (search width)
 };
 
+// Where the layer input x[r][col] lives: a dense row-major X (row stride n_in),
+// or the implicit im2col view of an NHWC image batch that unfold_conv would
+// materialize (conv.hpp:39-60): row r = (n, oy, ox) row-major over output
+// positions, column col = (dy*k + dx)*C + ch -> img[n][oy*s + dy][ox*s + dx][ch].
+// Both are "row base + column offset"; row_offset shifts r for row chunks.
+struct InputMap {
+    int conv;  // 0: dense X, 1: implicit im2col over an NHWC image batch
+    int out_h, out_w, H, W, C, k, s;
+    int64_t row_offset;
+};
+__host__ __device__ inline int64_t in_rowbase(const InputMap& m, int64_t r, int n_in) {
+    r += m.row_offset;
+    if (!m.conv) return r * n_in;
+    const int64_t per = static_cast<int64_t>(m.out_h) * m.out_w;
+    const int64_t n = r / per;
+    const int rem = static_cast<int>(r - n * per);
+    const int oy = rem / m.out_w, ox = rem - oy * m.out_w;
+    return ((n * m.H + static_cast<int64_t>(oy) * m.s) * m.W + static_cast<int64_t>(ox) * m.s) * m.C;
+}
+__host__ __device__ inline int in_coloff(const InputMap& m, int col) {
+    if (!m.conv) return col;
+    const int tap = col / m.C, ch = col - tap * m.C;
+    const int dy = tap / m.k, dx = tap - dy * m.k;
+    return (dy * m.W + dx) * m.C + ch;
+}
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -327,8 +353,11 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
 template <typename XT>
 __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
-                                                      int H, float4* __restrict__ W, int* __restrict__ O) {
+                                                      int H, float4* __restrict__ W, int* __restrict__ O,
+                                                      const InputMap im) {
     __shared__ XT xs[64][33];
+    __shared__ int64_t rbase[64];
+    __shared__ int coff[32];
     __shared__ XT thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
     extern __shared__ double inv[];  // G*G
@@ -336,31 +365,38 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
     for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
     const int p0 = blockIdx.y * 16;
-    for (int i = tid; i < 64 * 32; i += 256) {
-        const int r = i >> 5, c = i & 31;
-        const int64_t g = r0 + r;
-        const int col = 2 * p0 + c;
-        xs[r][c] = (g < rows && col < n_in) ? X[g * n_in + col] : XT(0);
-    }
-    __syncthreads();
     const int64_t tiles = rows_pad / sh.R;
+    // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
+    // (thresholds, points, G*G inverse areas) is amortized over many tiles
+    for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64; r0 < rows_pad; r0 += static_cast<int64_t>(gridDim.x) * 64) {
+        __syncthreads();  // previous tile's xs / rbase fully consumed
+        if (tid < 64) rbase[tid] = in_rowbase(im, r0 + tid, n_in);
+        if (tid < 32) coff[tid] = in_coloff(im, 2 * p0 + tid);
+        __syncthreads();
+        for (int i = tid; i < 64 * 32; i += 256) {
+            const int r = i >> 5, c = i & 31;
+            const int64_t g = r0 + r;
+            const int col = 2 * p0 + c;
+            xs[r][c] = (g < rows && col < n_in) ? X[rbase[r] + coff[c]] : XT(0);
+        }
+        __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int idx = tid + 256 * k;
-        const int r = idx & 63, pl = idx >> 6;
-        const int p = p0 + pl;
-        if (p >= pairs) continue;
-        const int64_t g = r0 + r;
-        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-        int packed = 0;
-        if (g < rows)
-            packed = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, sh.OT, H, w);
-        W[static_cast<size_t>(p) * rows_pad + g] = w;
-        const int64_t tile = g / sh.R;
-        const int qc = static_cast<int>(g - tile * sh.R);
-        O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
+        for (int k = 0; k < 4; ++k) {
+            const int idx = tid + 256 * k;
+            const int r = idx & 63, pl = idx >> 6;
+            const int p = p0 + pl;
+            if (p >= pairs) continue;
+            const int64_t g = r0 + r;
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            int packed = 0;
+            if (g < rows)
+                packed = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, sh.OT, H, w);
+            W[static_cast<size_t>(p) * rows_pad + g] = w;
+            const int64_t tile = g / sh.R;
+            const int qc = static_cast<int>(g - tile * sh.R);
+            O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
+        }
     }
 }
 
@@ -393,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float4* __restrict__ recW,
-                     const int* __restrict__ recO, int64_t rows_pad) {
+                     const int* __restrict__ recO, int64_t rows_pad, const InputMap im) {
     using Sh = FusedShape<OT, RT>;
     constexpr int R = Sh::R;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
@@ -477,24 +513,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane
     XT xa[Sh::LOC], xb[Sh::LOC];
     const XT* xrow[Sh::LOC];
-    const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0;
+    // float2 x-pair loads when both columns are adjacent and 8-byte aligned
+    const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0 && (!im.conv || (im.C & 1) == 0);
 #pragma unroll
     for (int k = 0; k < Sh::LOC; ++k) {
         const int q = k * 32 + lane;
         const int64_t r = row0 + warp * Sh::ROWS_W + q;
-        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && r < rows) ? X + r * n_in : nullptr;
+        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && r < rows) ? X + in_rowbase(im, r, n_in) : nullptr;
     }
     auto prefetch = [&](int p) {
+        const int c0 = in_coloff(im, 2 * p), c1 = im.conv ? in_coloff(im, 2 * p + 1) : c0 + 1;
 #pragma unroll
         for (int k = 0; k < Sh::LOC; ++k) {
             if (xrow[k]) {
                 if (sizeof(XT) == 4 && x_vec_ok) {
-                    const float2 v = __ldg(reinterpret_cast<const float2*>(xrow[k] + 2 * p));
+                    const float2 v = __ldg(reinterpret_cast<const float2*>(xrow[k] + c0));
                     xa[k] = v.x;
                     xb[k] = v.y;
                 } else {
-                    xa[k] = __ldg(xrow[k] + 2 * p);
-                    xb[k] = __ldg(xrow[k] + 2 * p + 1);
+                    xa[k] = __ldg(xrow[k] + c0);
+                    xb[k] = __ldg(xrow[k] + c1);
                 }
             } else {
                 xa[k] = xb[k] = XT(0);
@@ -638,12 +676,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // K4: narrow layers (n_out <= 4, e.g. the methane net's 128 -> 1 head). A
 // padded 16-wide output tile would waste >= 3/4 of every gather, so instead the
 // whole table, laid out [pair][node][NO] (NO = n_out rounded up to 1, 2 or 4),
-// is made resident in shared memory once per CTA (bulk copy), a warp walks
-// rows, each lane takes pairs p = lane, lane + 32, ... (row-contiguous x-pair
-// loads), locates, gathers its 4 corners and keeps a partial sum; a shuffle
-// tree reduces the 32 partials. Summation order: per lane over its pairs in
-// increasing p, then the fixed xor tree — deterministic, not the reference's
-// single chain (within the 1e-5 contract).
+// is made resident in shared memory once per CTA (bulk copy) and every lane
+// owns one row: it walks the pairs in order (x loaded 4 pairs = one 32-byte
+// sector at a time), locates and gathers its 4 corners per output. The
+// per-(row, output) arithmetic is exactly the general kernel's (same FMA
+// grouping, same pair order), so results are bitwise identical to it.
+constexpr int kNarrowThreads = 1024;
 __host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) {
     const uint32_t tab = static_cast<uint32_t>((G + 1) * (G + 1)) * pairs * NO * 4u;
     uint32_t o = (tab + 15u) & ~15u;
@@ -652,9 +690,10 @@ __host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) 
 }
 
 template <typename XT, int NO>
-__global__ void __launch_bounds__(256) narrow_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows,
-                                                     int n_in, int n_out, const float* __restrict__ table, float gamma,
-                                                     const __grid_constant__ GridConst gc) {
+__global__ void __launch_bounds__(kNarrowThreads, 1)
+    narrow_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
+                  const float* __restrict__ table, float gamma, const __grid_constant__ GridConst gc,
+                  const InputMap im) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G, pairs = n_in / 2, nodes = (G + 1) * (G + 1);
     const uint32_t tab_bytes = static_cast<uint32_t>(nodes) * pairs * NO * 4u;
@@ -667,10 +706,10 @@ __global__ void __launch_bounds__(256) narrow_kernel(const XT* __restrict__ X, X
     double* inv = reinterpret_cast<double*>(smem + o);
     o += static_cast<uint32_t>(G) * G * 8u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((o + 7u) & ~7u));
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
-    for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
-    for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
+    const int tid = threadIdx.x;
+    for (int k = tid; k < kMaxThr; k += kNarrowThreads) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k <= G; k += kNarrowThreads) pts[k] = gc.points[k];
+    for (int k = tid; k < G * G; k += kNarrowThreads) inv[k] = gc.inv_areas[k];
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
@@ -684,30 +723,37 @@ __global__ void __launch_bounds__(256) narrow_kernel(const XT* __restrict__ X, X
     __syncthreads();
     mbar_wait(bar, 0);
     const int rs1 = (G + 1) * NO;
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + warp; r < rows; r += static_cast<int64_t>(gridDim.x) * 8) {
-        float part[NO];
+    const bool vec4 = sizeof(XT) == 4 && !im.conv && (n_in & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * kNarrowThreads + tid; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * kNarrowThreads) {
+        float acc[NO];
 #pragma unroll
-        for (int q = 0; q < NO; ++q) part[q] = 0.f;
-        const XT* xr = X + r * n_in;
-        for (int p = lane; p < pairs; p += 32) {
+        for (int q = 0; q < NO; ++q) acc[q] = 0.f;
+        const XT* xr = X + in_rowbase(im, r, n_in);
+        auto one_pair = [&](int p, XT x1, XT x2) {
             float4 w;
-            const int off = locate_record<XT>(xr[2 * p], xr[2 * p + 1], thr, pts, inv, G, gc.L, NO, G, w);
+            const int off = locate_record<XT>(x1, x2, thr, pts, inv, G, gc.L, NO, G, w);
             const float* b = tab + static_cast<size_t>(p) * nodes * NO + off;
 #pragma unroll
             for (int q = 0; q < NO; ++q)
-                part[q] += fmaf(w.w, b[rs1 + NO + q], fmaf(w.z, b[NO + q], fmaf(w.y, b[rs1 + q], w.x * b[q])));
+                acc[q] += fmaf(w.w, b[rs1 + NO + q], fmaf(w.z, b[NO + q], fmaf(w.y, b[rs1 + q], w.x * b[q])));
+        };
+        int p = 0;
+        if (vec4) {
+            for (; p + 4 <= pairs; p += 4) {  // one 32-byte sector of the row = 4 pairs
+                const float4 u = __ldg(reinterpret_cast<const float4*>(xr + 2 * p));
+                const float4 v = __ldg(reinterpret_cast<const float4*>(xr + 2 * p + 4));
+                one_pair(p, u.x, u.y);
+                one_pair(p + 1, u.z, u.w);
+                one_pair(p + 2, v.x, v.y);
+                one_pair(p + 3, v.z, v.w);
+            }
         }
+        for (; p < pairs; ++p) one_pair(p, xr[in_coloff(im, 2 * p)], xr[in_coloff(im, 2 * p + 1)]);
+        XT* yr = Y + r * n_out;
 #pragma unroll
         for (int q = 0; q < NO; ++q)
-#pragma unroll
-            for (int m = 16; m > 0; m >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], m);
-        if (lane < n_out) {
-            float v = part[0];
-#pragma unroll
-            for (int q = 1; q < NO; ++q)
-                if (lane == q) v = part[q];
-            Y[r * n_out + lane] = static_cast<XT>(v * gamma);
-        }
+            if (q < n_out) yr[q] = static_cast<XT>(acc[q] * gamma);
     }
 }
 

@@ -8,7 +8,7 @@ namespace lmkan_b200 {
 
 template <int OT, int RT, typename XT, int MODE, bool SLAB>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                           const float4* recW, const int* recO, cudaStream_t st) {
+                           const float4* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
@@ -19,30 +19,30 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
     }
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
     kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
-                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad);
+                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im);
     return cudaGetLastError();
 }
 
 template <int OT, typename XT, int MODE, bool SLAB>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                            const float4* recW, const int* recO, cudaStream_t st) {
+                            const float4* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     switch (pl.RT) {
-        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
-        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
-        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, st);
+        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
+        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
+        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
     }
 }
 
 template <int OT, typename XT>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                              const float4* recW, const int* recO, cudaStream_t st) {
+                              const float4* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     if (pl.mode == kModeGlobal)
-        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, st);
+        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, st);
     if (pl.mode == kModeStaged)
-        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, st)
-                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, st);
-    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, st)
-                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, st);
+        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, st)
+                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, st);
+    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, im, st)
+                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, im, st);
 }
 
 }  // namespace lmkan_b200
@@ -50,7 +50,9 @@ cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X
 #define LMKAN_B200_INSTANTIATE_GATHER(OT)                                                                        \
     template cudaError_t lmkan_b200::launch_gather<OT, float>(const lmkan_b200_layer*, const lmkan_b200::Plan&, \
                                                               const float*, float*, int64_t, const float4*,      \
-                                                              const int*, cudaStream_t);                         \
+                                                              const int*, const lmkan_b200::InputMap&,           \
+                                                              cudaStream_t);                                     \
     template cudaError_t lmkan_b200::launch_gather<OT, double>(const lmkan_b200_layer*,                          \
                                                                const lmkan_b200::Plan&, const double*, double*,  \
-                                                               int64_t, const float4*, const int*, cudaStream_t);
+                                                               int64_t, const float4*, const int*,               \
+                                                               const lmkan_b200::InputMap&, cudaStream_t);

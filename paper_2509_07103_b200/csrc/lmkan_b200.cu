@@ -129,7 +129,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
               force_s = env_int("LMKAN_B200_SLABS", 0);
     if (L->narrow) {
-        const int64_t ctas = std::min<int64_t>(kNumSMs, (rows + 7) / 8);
+        const int64_t ctas = std::min<int64_t>(kNumSMs, (rows + kNarrowThreads - 1) / kNarrowThreads);
         out = Plan{L->OT, 1, 1, kModeNarrow, 1, shape_rt(16, 4), narrow_smem_bytes(L->G, L->pairs, L->OT), ctas,
                    rows, 1};
         return static_cast<int>(out.smem) <= smem_cap;
@@ -179,7 +179,7 @@ size_t record_scratch_cap() { return static_cast<size_t>(env_int("LMKAN_B200_MAX
 // One launch group (K1 + K2 in staged mode, K3 otherwise) over `rows` rows.
 template <typename XT, int NO>
 cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                          cudaStream_t st) {
+                          const InputMap& im, cudaStream_t st) {
     static int configured[64] = {0};
     if (!configured[L->device & 63]) {
         cudaError_t e =
@@ -187,19 +187,19 @@ cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X
         if (e != cudaSuccess) return e;
         configured[L->device & 63] = 1;
     }
-    narrow_kernel<XT, NO><<<static_cast<unsigned>(pl.row_tiles), 256, pl.smem, st>>>(
-        X, Y, rows, L->n_in, L->n_out, L->table, static_cast<float>(L->gamma), L->gc);
+    narrow_kernel<XT, NO><<<static_cast<unsigned>(pl.row_tiles), kNarrowThreads, pl.smem, st>>>(
+        X, Y, rows, L->n_in, L->n_out, L->table, static_cast<float>(L->gamma), L->gc, im);
     return cudaGetLastError();
 }
 
 template <typename XT>
-int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
-                 cudaEvent_t ev_begin, cudaEvent_t ev_end) {
+int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows, const InputMap& im,
+                 cudaStream_t st, cudaEvent_t ev_begin, cudaEvent_t ev_end) {
     if (pl.mode == kModeNarrow) {
         if (ev_begin) cudaEventRecord(ev_begin, st);
-        const cudaError_t e = L->OT == 1   ? launch_narrow<XT, 1>(L, pl, X, Y, rows, st)
-                              : L->OT == 2 ? launch_narrow<XT, 2>(L, pl, X, Y, rows, st)
-                                           : launch_narrow<XT, 4>(L, pl, X, Y, rows, st);
+        const cudaError_t e = L->OT == 1   ? launch_narrow<XT, 1>(L, pl, X, Y, rows, im, st)
+                              : L->OT == 2 ? launch_narrow<XT, 2>(L, pl, X, Y, rows, im, st)
+                                           : launch_narrow<XT, 4>(L, pl, X, Y, rows, im, st);
         if (ev_end) cudaEventRecord(ev_end, st);
         if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: narrow kernel launch");
         return LMKAN_B200_OK;
@@ -216,10 +216,12 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
             cudaFreeAsync(recW, st);
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
-        dim3 g1(static_cast<unsigned>(pl.rows_pad / 64), static_cast<unsigned>((L->pairs + 15) / 16));
+        const int64_t py = (L->pairs + 15) / 16;
+        const int64_t gx = std::min<int64_t>(pl.rows_pad / 64, std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
+        dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
         records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
-                                                                            pl.sh, H, recW, recO);
+                                                                            pl.sh, H, recW, recO, im);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(recW, st);
@@ -230,9 +232,9 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
     switch (L->OT) {
-        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, recW, recO, st); break;
-        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, recW, recO, st); break;
-        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, recW, recO, st); break;
+        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
+        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
+        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
     }
     if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
@@ -243,7 +245,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
 
 template <typename XT>
 int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
-                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr) {
+                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, InputMap im = InputMap{}) {
     if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
     if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
     if (rows == 0) return LMKAN_B200_OK;
@@ -269,7 +271,9 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
         if (n != rows && !make_plan(L, n, cap, pc))
             return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
         const bool first = r0 == 0, last = r0 + n >= rows;
-        if (int rc = forward_rows<XT>(L, pc, X + r0 * L->n_in, Y + r0 * L->n_out, n, st, first ? ev_begin : nullptr,
+        InputMap imc = im;
+        imc.row_offset = r0;
+        if (int rc = forward_rows<XT>(L, pc, X, Y + r0 * L->n_out, n, imc, st, first ? ev_begin : nullptr,
                                       last ? ev_end : nullptr))
             return rc;
     }
@@ -585,6 +589,30 @@ int lmkan_b200_forward_f32_timed(const lmkan_b200_layer* L, const float* X, floa
                                  void* ev_begin, void* ev_end) {
     return forward_device<float>(L, X, Y, rows, static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev_begin),
                                  static_cast<cudaEvent_t>(ev_end));
+}
+int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,
+                                int s, float* Y, void* stream) {
+    // argument checks of unfold_conv (conv.hpp:40-45), then the layer width check (layer.hpp:110)
+    if (!L) return fail(LMKAN_B200_EINVAL, "conv_forward: null layer");
+    if (k < 1 || s < 1) return fail(LMKAN_B200_EINVAL, "unfold_conv: k and s must be positive");
+    if (k > H || k > W) return fail(LMKAN_B200_EINVAL, "unfold_conv: kernel larger than image");
+    if ((H - k) % s != 0 || (W - k) % s != 0)
+        return fail(LMKAN_B200_EINVAL, "unfold_conv: (H-k) and (W-k) must be divisible by the stride");
+    if (N < 0 || C < 1) return fail(LMKAN_B200_EINVAL, "conv_forward: bad image batch shape");
+    if (static_cast<int64_t>(k) * k * C != L->n_in)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: expected width " + std::to_string(L->n_in) + ", got " +
+                                           std::to_string(static_cast<int64_t>(k) * k * C));
+    InputMap im{};
+    im.conv = 1;
+    im.out_h = (H - k) / s + 1;
+    im.out_w = (W - k) / s + 1;
+    im.H = H;
+    im.W = W;
+    im.C = C;
+    im.k = k;
+    im.s = s;
+    const int64_t rows = static_cast<int64_t>(N) * im.out_h * im.out_w;
+    return forward_device<float>(L, img, Y, rows, static_cast<cudaStream_t>(stream), nullptr, nullptr, im);
 }
 int lmkan_b200_forward_f64(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, void* stream) {
     return forward_device<double>(L, X, Y, rows, static_cast<cudaStream_t>(stream));

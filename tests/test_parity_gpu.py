@@ -306,7 +306,7 @@ def test_cfg5_shape_output_slice(torch, pkg, oracle):
                                                (2, 4, 5, 100), (200, 1, 12, 513)])
 def test_narrow_kernel(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows):
     """n_out <= 4 layers run the narrow kernel (whole table in shared memory,
-    lanes over pairs); parity vs the oracle and vs the padded general path."""
+    one row per lane); parity vs the oracle, bitwise vs the padded general path."""
     P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in + 7 * n_out)
     layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 0.9)
     assert layer.plan(rows)["mode"] == "narrow"
@@ -318,4 +318,50 @@ def test_narrow_kernel(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows):
     monkeypatch.setenv("LMKAN_B200_NARROW", "0")
     wide = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 0.9)
     assert wide.plan(rows)["mode"] != "narrow"
-    assert _mixed(wide.forward(Xd).cpu().numpy(), ref).max() <= TOL
+    # same per-(row, output) arithmetic and pair order as the general kernel
+    assert np.array_equal(wide.forward(Xd).cpu().numpy(), Y)
+
+
+def _unfold(img, k, s):
+    """unfold_conv (conv.hpp:39-60) restated in numpy: rows over (n, oy, ox),
+    columns (dy*k + dx)*C + ch."""
+    N, H, W, C = img.shape
+    oh, ow = (H - k) // s + 1, (W - k) // s + 1
+    cols = []
+    for dy in range(k):
+        for dx in range(k):
+            cols.append(img[:, dy:dy + s * (oh - 1) + 1:s, dx:dx + s * (ow - 1) + 1:s, :])
+    return np.concatenate(cols, axis=-1).reshape(N * oh * ow, k * k * C), oh, ow
+
+
+@pytest.mark.parametrize("N,H,W,C,k,s,n_out,G", [
+    (4, 10, 10, 16, 3, 1, 16, 16),   # CIFAR stage-1 geometry, small batch
+    (2, 9, 9, 2, 3, 3, 7, 8),
+    (3, 8, 8, 6, 2, 2, 40, 5),
+    (2, 7, 9, 3, 2, 1, 10, 6),       # odd C: x pairs straddle taps
+    (2, 6, 6, 4, 3, 1, 2, 12),       # narrow head (n_out <= 4)
+])
+def test_conv_implicit_im2col(torch, pkg, oracle, N, H, W, C, k, s, n_out, G):
+    rng = np.random.default_rng(N * 100 + C)
+    img = rng.standard_normal((N, H, W, C)).astype(np.float32)
+    n_in = k * k * C
+    P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    Y = layer.conv_forward(torch.from_numpy(img).cuda(), k, s)
+    patches, oh, ow = _unfold(img, k, s)
+    assert Y.shape == (N, oh, ow, n_out)  # fold_output layout (conv.hpp:63-71)
+    Yx = layer.forward(torch.from_numpy(np.ascontiguousarray(patches)).cuda())
+    assert torch.equal(Y.reshape(-1, n_out), Yx)  # same rows, same kernel, same order
+    ref = oracle.forward(G, P.astype(np.float64), patches.astype(np.float64), 1.0)
+    assert _mixed(Y.reshape(-1, n_out).cpu().numpy(), ref).max() <= TOL
+
+
+def test_conv_argument_errors(torch, pkg):
+    layer = pkg.Layer.random(2 * 2 * 4, 8, 5)
+    img = torch.zeros((1, 7, 7, 4), device="cuda")
+    with pytest.raises(ValueError, match="divisible by the stride"):
+        layer.conv_forward(img, 2, 2)
+    with pytest.raises(ValueError, match="kernel larger than image"):
+        layer.conv_forward(torch.zeros((1, 1, 1, 4), device="cuda"), 2, 1)
+    with pytest.raises(ValueError, match="expected width 16, got 36"):
+        layer.conv_forward(img, 3, 1)
