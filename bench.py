@@ -40,6 +40,8 @@ CONFIGS = {
     4: dict(name="cfg4: lmKAN 3x3 conv (implicit im2col), 144->16, G=16, 256 images 32x32x16 (zero-padded 34x34)",
             layers=[(144, 16)], G=16, batch=262144, conv=dict(N=256, H=34, W=34, C=16, k=3, s=1)),
 }
+CONFIGS[5] = dict(name="cfg5: wide lmKAN layer 8192->8192, G=32, batch 262144, output-sharded",
+                  layers=[(8192, 8192)], G=32, batch=262144, out_sharded=True)
 METRIC = "lmKAN layer fwd samples/s at 1/2/4/8 B200; achieved GB/s vs HBM roofline"
 
 
@@ -218,6 +220,9 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shards", type=int, default=0,
+                    help="config 5: number of output shards (default: world size); with one process, "
+                         "measures shard 0 of K (what each of K GPUs computes) without the all-gather")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -241,8 +246,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G = cfg["G"]
     B = cfg["batch"]
-    layers = [pkg.Layer.random(n_in, n_out, G, seed=1000 + i, gamma=1.0, device=local)
-              for i, (n_in, n_out) in enumerate(cfg["layers"])]
+    out_sharded = bool(cfg.get("out_sharded"))
+    shards = (args.shards or ws) if out_sharded else 1
+    if out_sharded:
+        from paper_2509_07103_b200 import sharding
+        n_in0, n_out0 = cfg["layers"][0]
+        ob, oe = sharding.shard_range(n_out0, rank % shards, shards, align=16)
+        layers = [pkg.Layer.random(n_in0, n_out0, G, seed=1000, gamma=1.0, device=local, out_range=(ob, oe))]
+        cfg = dict(cfg, layers=[(n_in0, oe - ob)])  # this rank's local layer
+        Yfull = torch.empty((B, n_out0), device=f"cuda:{local}") if ws > 1 else None
+    else:
+        layers = [pkg.Layer.random(n_in, n_out, G, seed=1000 + i, gamma=1.0, device=local)
+                  for i, (n_in, n_out) in enumerate(cfg["layers"])]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + rank)
     conv = cfg.get("conv")
     if conv:  # NHWC image batch; patch rows are formed on the fly (implicit im2col)
@@ -282,6 +297,8 @@ def main():
             else:
                 lay.forward_into_timed(cur, out, gev[i][li][0], gev[i][li][1], stream)
             cur = out
+        if out_sharded and ws > 1:  # NCCL all-gather of the output-column shards
+            sharding.gather_columns(acts[-1], n_out0, ws, rank, align=16, out=Yfull)
 
     for _ in range(args.warmup):
         step()
@@ -309,7 +326,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / K
-    value = ws * B / (ms_per_step / 1e3)
+    # batch-sharded configs: every rank runs its own B rows (weak scaling);
+    # config 5: all ranks cooperate on the same B rows (strong scaling)
+    value = (B if out_sharded else ws * B) / (ms_per_step / 1e3)
     kernel_ms = statistics.mean(gather_ms)  # gather kernel(s) of one step, event-timed on the launch stream
     launches_per_step = sum(l.plan(B)["launches"] for l in layers)
 
@@ -351,7 +370,7 @@ def main():
         dt = float(te.item())
         h2d = X.numel() * 4
         d2h = B * n_last * 4
-        e2e = {"value": ws * B / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        e2e = {"value": (B if out_sharded else ws * B) / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": dt * 1e3,
                "timer": "host wall clock around H2D + forward + D2H + host read (public API)"}
 
@@ -366,8 +385,15 @@ def main():
     plan = layers[0].plan(B)
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        tables = [lay.read_table() for lay in layers]
-        v, cores, sample, kind = cpu_reference(cfg, tables)
+        if out_sharded:  # 146 GB fp64 table does not fit the host: time a 16-output slice, scale by cost ~ n_out
+            n_in0 = cfg["layers"][0][0]
+            sl = pkg.Layer.random(n_in0, n_out0, G, seed=1000, gamma=1.0, device=local, out_range=(0, 16))
+            v, cores, sample, kind = cpu_reference(dict(cfg, layers=[(n_in0, 16)]), [sl.read_table()], budget_s=10)
+            v = v * 16 / n_out0
+            sample += f"; 16-output slice of the {n_out0}-output layer, samples/s scaled by 16/{n_out0} (cost is linear in n_out)"
+        else:
+            tables = [lay.read_table() for lay in layers]
+            v, cores, sample, kind = cpu_reference(cfg, tables)
         cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind, "sample": sample,
                "cpu_model": host_cpu_model(), "threads_env": "LMKAN_THREADS=nproc"}
     fmas = B * sum(fma_per_row(a, b) for a, b in cfg["layers"])
@@ -380,12 +406,16 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if out_sharded else "weak",
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic: X ~ N(0,1) (torch CUDA generator), table ~ N(0, 1/pairs) from a device counter RNG",
         "config": {"workload": cfg["name"], "layers": cfg["layers"], "G": G, "batch_per_gpu": B,
-                   "global_batch": ws * B, "parallelism": f"dp{ws} (batch rows, no collective)",
+                   "global_batch": B if out_sharded else ws * B,
+                   "parallelism": (f"output-sharded over {shards} (this run: {ws} process(es); shard "
+                                   f"{rank % shards}, n_out_local={cfg['layers'][0][1]}"
+                                   f"{', NCCL all-gather of Y columns' if ws > 1 else ', no all-gather: single-rank shard measurement'})"
+                                   if out_sharded else f"dp{ws} (batch rows, no collective)"),
                    "l2": "inputs larger than L2: X %.0f MB, table %.0f MB vs 126 MB L2" % (
                        B * cfg["layers"][0][0] * 4 / 1e6, sum(l.table_bytes for l in layers) / 1e6),
                    "kernel_plan": plan},
@@ -414,10 +444,18 @@ def reference_arm(args, cfg, ws):
     import numpy as np
     G = cfg["G"]
     rng = np.random.default_rng(1000)
+    scale, run_cfg = 1.0, cfg
+    if cfg.get("out_sharded"):  # the fp64 table (292 GB) does not fit the host: 16-output slice, scaled
+        n_in0, n_out0 = cfg["layers"][0]
+        run_cfg = dict(cfg, layers=[(n_in0, 16)])
+        scale = 16 / n_out0
     tables = [(rng.standard_normal(((G + 1) ** 2 * (a // 2) * b)).astype(np.float32).astype(np.float64)
-               / np.sqrt(a // 2)).reshape(G + 1, G + 1, a // 2, b) for a, b in cfg["layers"]]
+               / np.sqrt(a // 2)).reshape(G + 1, G + 1, a // 2, b) for a, b in run_cfg["layers"]]
     budget = max(6.0, min(60.0, 2.0 * (args.steps + args.warmup)))
-    v, cores, sample, kind = cpu_reference(cfg, tables, budget_s=budget)
+    v, cores, sample, kind = cpu_reference(run_cfg, tables, budget_s=budget)
+    if scale != 1.0:
+        v *= scale
+        sample += f"; 16-output slice, samples/s scaled by {scale:g} (cost is linear in n_out)"
     out = {
         "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": cfg["batch"] / v * 1e3, "higher_is_better": True,

@@ -374,11 +374,18 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
         if (tid < 64) rbase[tid] = in_rowbase(im, r0 + tid, n_in);
         if (tid < 32) coff[tid] = in_coloff(im, 2 * p0 + tid);
         __syncthreads();
-        for (int i = tid; i < 64 * 32; i += 256) {
+        XT v[8];  // all 8 loads of this thread in flight before any store
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int i = tid + 256 * t;
             const int r = i >> 5, c = i & 31;
-            const int64_t g = r0 + r;
             const int col = 2 * p0 + c;
-            xs[r][c] = (g < rows && col < n_in) ? X[rbase[r] + coff[c]] : XT(0);
+            v[t] = (r0 + r < rows && col < n_in) ? __ldg(X + rbase[r] + coff[c]) : XT(0);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int i = tid + 256 * t;
+            xs[i >> 5][i & 31] = v[t];
         }
         __syncthreads();
 #pragma unroll

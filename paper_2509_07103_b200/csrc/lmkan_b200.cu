@@ -217,7 +217,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
         const int64_t py = (L->pairs + 15) / 16;
-        const int64_t gx = std::min<int64_t>(pl.rows_pad / 64, std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
+        const int64_t gx = std::min<int64_t>(pl.rows_pad / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
         records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
