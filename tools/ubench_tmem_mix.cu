@@ -6,6 +6,7 @@
 // the mix. Also a pure .x4 / .x8 TMEM gather for the ceiling.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t lcg(uint32_t& s) {
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(512, 1) mix_bench(int iters, uint32_t seed, fl
         uint32_t r[32];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // 4 rows per iteration
-            const uint32_t n1 = (lcg(s) >> 20) & 255, n2 = (lcg(s) >> 20) & 255;
+            const uint32_t n1 = (lcg(s) >> 20) & 255, n2 = (lcg(s) >> 20) & 254;
             if (MODE == 0 || MODE == 2) {  // SMEM: corners (n1, n1+1) and, in mode 0, (n2, n2+1)
                 const float2 a = sh[n1 * 32 + lane], b = sh[(n1 + 1) * 32 + lane];
                 acc += a.x + a.y + b.x + b.y;
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(512, 1) mix_bench(int iters, uint32_t seed, fl
                              : "r"(base + lane_base + 2 * n2));
             }
             if (MODE == 1) {
-                const uint32_t n3 = (lcg(s) >> 20) & 255;
+                const uint32_t n3 = (lcg(s) >> 20) & 254;
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                              : "=r"(r[16 + 4 * k]), "=r"(r[17 + 4 * k]), "=r"(r[18 + 4 * k]), "=r"(r[19 + 4 * k])
                              : "r"(base + lane_base + 2 * n3));
@@ -111,12 +112,14 @@ void run(const char* name, int sms, double bytes_per_row) {
     cudaFree(cyc);
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int mode = argc > 1 ? atoi(argv[1]) : -1;
+    setvbuf(stdout, nullptr, _IONBF, 0);
     printf("SMs=%d (a 'row' = 4 corners x 64 outputs x 4 B = 1024 B)\n", sms);
-    run<0>("smem only: 4 x LDS.64", sms, 1024);
-    run<1>("tmem only: 2 x ld.32x32b.x4", sms, 1024);
-    run<2>("mix: 2 x LDS.64 + 1 x ld.x4", sms, 1024);
+    if (mode < 0 || mode == 0) run<0>("smem only: 4 x LDS.64", sms, 1024);
+    if (mode < 0 || mode == 1) run<1>("tmem only: 2 x ld.32x32b.x4", sms, 1024);
+    if (mode < 0 || mode == 2) run<2>("mix: 2 x LDS.64 + 1 x ld.x4", sms, 1024);
     return 0;
 }
