@@ -152,11 +152,13 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, in
  * RT = rows per thread, NBUF = sheet buffers, rows_per_cta), the number of
  * kernel launches one forward issues, the mode (0 = fused locate+gather,
  * 1 = staged: cell-record kernel + gather kernel, 2 = global-sheet fallback)
- * and the number of i1-slabs a sheet is streamed in. Environment overrides
- * for experiments: LMKAN_B200_MODE=fused|staged|global, LMKAN_B200_RT,
- * LMKAN_B200_NBUF, LMKAN_B200_SLABS, LMKAN_B200_OT (at layer creation). */
+ * the number of i1-slabs a sheet is streamed in and the warps per CTA (16,
+ * fewer for batches too small to fill the GPU). Environment overrides for
+ * experiments: LMKAN_B200_MODE=fused|staged|global, LMKAN_B200_RT,
+ * LMKAN_B200_NBUF, LMKAN_B200_SLABS, LMKAN_B200_NW, LMKAN_B200_OT (at layer
+ * creation). Any output pointer may be NULL. */
 int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
-                    int* nbuf, int* rows_per_cta, int* launches, int* mode, int* slabs);
+                    int* nbuf, int* rows_per_cta, int* launches, int* mode, int* slabs, int* warps_per_cta);
 
 #ifdef __cplusplus
 }

@@ -219,9 +219,10 @@ class Layer:
         return out
 
     def plan(self, rows: int) -> dict:
-        v = [C.c_int() for _ in range(7)]
+        v = [C.c_int() for _ in range(8)]
         check(lib.lmkan_b200_plan(self._h, int(rows), *[C.byref(x) for x in v]))
-        d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode", "slabs"],
+        d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode", "slabs",
+                      "warps_per_cta"],
                      [x.value for x in v]))
         d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow"}[d["mode"]]
         return d

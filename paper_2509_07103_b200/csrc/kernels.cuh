@@ -196,11 +196,12 @@ __global__ void __launch_bounds__(256) locate_kernel(const XT* __restrict__ X, i
     }
 }
 
-// Fast cell index: an fp32 sigma estimate (MUFU exp) is corrected by one
-// threshold step either way and then VERIFIED against the threshold table
-// (t_k = thr[k-1]); only if the verification fails (NaN, or an estimate off by
-// more than one cell) does it fall back to the exact binary search. The result
-// is therefore always #{k : x >= t_k}, i.e. the reference interval_index.
+// Fast cell index: an fp32 sigma estimate (MUFU exp) is VERIFIED against the
+// two thresholds bracketing it (t_k = thr[k-1]; thr[G-1] is the NaN padding, so
+// the top cell's upper test !(x >= NaN) always holds). Only if the verification
+// fails (NaN input, or an estimate off by a cell: ~1e-6 of N(0,1) draws) does it
+// fall back to the exact binary search. The result is therefore always
+// #{k : x >= t_k}, i.e. the reference interval_index.
 template <typename XT>
 __device__ __forceinline__ int cell_index_fast(XT x, const XT* thr, int G, int L) {
     const float xf = static_cast<float>(x);
@@ -208,9 +209,9 @@ __device__ __forceinline__ int cell_index_fast(XT x, const XT* thr, int G, int L
     const float s = xf > 0.f ? 1.f - 0.5f * e : 0.5f * e;
     int i = static_cast<int>(s * static_cast<float>(G));
     i = i < 0 ? 0 : (i > G - 1 ? G - 1 : i);
-    if (i > 0 && !(x >= thr[i - 1])) --i;
-    else if (i < G - 1 && x >= thr[i]) ++i;
-    const bool ok = (i == 0 || x >= thr[i - 1]) && (i == G - 1 || x < thr[i]);
+    const XT lo = thr[i > 0 ? i - 1 : 0];
+    const XT hi = thr[i];
+    const bool ok = (i == 0 || x >= lo) && !(x >= hi) && x == x;
     return ok ? i : cell_index<XT>(x, thr, L);
 }
 // Slab split of a sheet along i1: slab s holds the node rows
@@ -258,37 +259,43 @@ enum : int {
 };
 
 // Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
-template <int OT, int RT>
+template <int OT, int RT, int NW = kWarps>
 struct FusedShape {
     static constexpr int LPR = OT / 4;               // lanes covering one row's OT outputs (float4 each)
     static constexpr int RPW = 32 / LPR;             // rows per warp per gather instruction
     static constexpr int ROWS_W = RPW * RT;          // rows owned by one warp
     static constexpr int LOC = (ROWS_W + 31) / 32;   // cells each lane locates per pair (fused mode)
-    static constexpr int R = kWarps * ROWS_W;        // rows per CTA
+    static constexpr int R = NW * ROWS_W;             // rows per CTA
     static constexpr int OSTRIDE = RT + (RPW > 2 ? 4 : 0);  // padded per-lane-group offset run (bank spread)
-    static constexpr int OBLK = kWarps * RPW * OSTRIDE;     // offset ints per CTA per pair
+    static constexpr int OBLK = NW * RPW * OSTRIDE;         // offset ints per CTA per pair
 };
 // Runtime twin of FusedShape for host code / K1.
 struct ShapeRT {
-    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK;
+    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK, NW;
+    int lgRPW, lgROWS_W, lgR;  // RPW, ROWS_W, R are powers of two (OT, RT, NW are)
 };
-__host__ __device__ inline ShapeRT shape_rt(int OT, int RT) {
+__host__ __device__ constexpr int ilog2(int v) { return v > 1 ? 1 + ilog2(v >> 1) : 0; }
+__host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps) {
     ShapeRT s;
     s.OT = OT;
     s.RT = RT;
+    s.NW = NW;
     s.LPR = OT / 4;
     s.RPW = 32 / s.LPR;
     s.ROWS_W = s.RPW * RT;
-    s.R = kWarps * s.ROWS_W;
+    s.R = NW * s.ROWS_W;
     s.OSTRIDE = RT + (s.RPW > 2 ? 4 : 0);
-    s.OBLK = kWarps * s.RPW * s.OSTRIDE;
+    s.OBLK = NW * s.RPW * s.OSTRIDE;
+    s.lgRPW = ilog2(s.RPW);
+    s.lgROWS_W = ilog2(s.ROWS_W);
+    s.lgR = ilog2(s.R);
     return s;
 }
 // Position of CTA-local row qc's node offset inside the CTA's offset block: the
 // RT rows a lane group gathers are contiguous, so a thread loads them as int4s.
 __host__ __device__ inline int offset_slot(const ShapeRT& s, int qc) {
-    const int warp = qc / s.ROWS_W, q = qc % s.ROWS_W;
-    const int sub = q % s.RPW, j = q / s.RPW;
+    const int warp = qc >> s.lgROWS_W, q = qc & (s.ROWS_W - 1);
+    const int sub = q & (s.RPW - 1), j = q >> s.lgRPW;
     return (warp * s.RPW + sub) * s.OSTRIDE + j;
 }
 
@@ -308,8 +315,9 @@ struct FusedSmem {
         off_cnt, total;
     int nrec;
 };
-__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1) {
-    const ShapeRT sh = shape_rt(OT, RT);
+__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1,
+                                                       int NW = kWarps) {
+    const ShapeRT sh = shape_rt(OT, RT, NW);
     const int H = (G + S - 1) / S;
     const int nb = nbuf > 0 ? nbuf : 1;
     FusedSmem s;
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
     for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
     const int p0 = blockIdx.y * 16;
-    const int64_t tiles = rows_pad / sh.R;
+    const int64_t tiles = rows_pad >> sh.lgR;
     // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
     // (thresholds, points, G*G inverse areas) is amortized over many tiles
     for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64; r0 < rows_pad; r0 += static_cast<int64_t>(gridDim.x) * 64) {
@@ -395,13 +403,14 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
             const int p = p0 + pl;
             if (p >= pairs) continue;
             const int64_t g = r0 + r;
+            if (g >= rows_pad) continue;  // row tiles (R) may be shorter than the 64-row X tile
             float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
             int packed = 0;
             if (g < rows)
                 packed = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, sh.OT, H, w);
             W[static_cast<size_t>(p) * rows_pad + g] = w;
-            const int64_t tile = g / sh.R;
-            const int qc = static_cast<int>(g - tile * sh.R);
+            const int64_t tile = g >> sh.lgR;
+            const int qc = static_cast<int>(g & (sh.R - 1));
             O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
         }
     }
@@ -431,20 +440,21 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT, int MODE, bool SLAB>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float4* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im) {
-    using Sh = FusedShape<OT, RT>;
+    using Sh = FusedShape<OT, RT, NW>;
     constexpr int R = Sh::R;
+    constexpr int NT = NW * 32;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
     const int H = (G + S - 1) / S;
-    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S);
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW);
     float* sheets = reinterpret_cast<float*>(smem);
     float4* rec_w = reinterpret_cast<float4*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
@@ -467,9 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int units = pairs * S;
 
     if constexpr (MODE != kModeStaged) {
-        for (int k = tid; k < kMaxThr; k += kThreads) thr[k] = thr_of<XT>(gc)[k];
-        for (int k = tid; k <= G; k += kThreads) pts[k] = gc.points[k];
-        for (int k = tid; k < G * G; k += kThreads) inv[k] = gc.inv_areas[k];
+        for (int k = tid; k < kMaxThr; k += NT) thr[k] = thr_of<XT>(gc)[k];
+        for (int k = tid; k <= G; k += NT) pts[k] = gc.points[k];
+        for (int k = tid; k < G * G; k += NT) inv[k] = gc.inv_areas[k];
     }
     uint64_t policy = 0, policy_rec = 0;
     if constexpr (kSmemSheet) {
@@ -547,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
     auto locate = [&]() {
-        const ShapeRT shp = shape_rt(OT, RT);
+        const ShapeRT shp = shape_rt(OT, RT, NW);
 #pragma unroll
         for (int k = 0; k < Sh::LOC; ++k) {
             const int q = k * 32 + lane;
@@ -637,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) {
                 const int slot = u % nbuf;
                 __threadfence_block();
-                if (atomicAdd(&cnt[slot], 1u) == kWarps - 1) {  // last warp out refills the slot
+                if (atomicAdd(&cnt[slot], 1u) == NW - 1) {  // last warp out refills the slot
                     cnt[slot] = 0;
                     if (u + nbuf < units) {
                         fence_proxy_async();

@@ -6,10 +6,10 @@
 
 namespace lmkan_b200 {
 
-template <int OT, int RT, typename XT, int MODE, bool SLAB>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
                            const float4* recW, const int* recO, const InputMap& im, cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB>;
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
     if (!configured[dev]) {
@@ -18,7 +18,7 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
         configured[dev] = 1;
     }
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
-    kern<<<grid, kThreads, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
+    kern<<<grid, NW * 32, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
                                            static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im);
     return cudaGetLastError();
 }
@@ -26,6 +26,15 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
 template <int OT, typename XT, int MODE, bool SLAB>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
                             const float4* recW, const int* recO, const InputMap& im, cudaStream_t st) {
+    if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT = 4) so the grid still spans the GPU
+        switch (pl.sh.NW) {
+            case 8: return launch_fused_t<OT, 4, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, st);
+            case 4: return launch_fused_t<OT, 4, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, st);
+            case 2: return launch_fused_t<OT, 4, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, st);
+            case 1: return launch_fused_t<OT, 4, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, st);
+            default: break;
+        }
+    }
     switch (pl.RT) {
         case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
         case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);

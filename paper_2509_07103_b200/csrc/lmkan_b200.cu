@@ -140,7 +140,12 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
         if (!std::strcmp(e, "staged")) force_mode = kModeStaged;
         if (!std::strcmp(e, "global")) force_mode = kModeGlobal;
     }
-    const int pref = L->n_ot >= 3 ? kModeStaged : kModeFused;
+    // staged when >= 3 output tiles re-read the cells, or when the batch is too
+    // small to give every SM a 16-warp CTA (the per-pair locate then sits on the
+    // critical path of the few rows each CTA owns; measured 32 vs 47 us at cfg1)
+    const bool small = ((rows + shape_rt(L->OT, kRTChoices[2]).R - 1) / shape_rt(L->OT, kRTChoices[2]).R) * L->n_ot <
+                       kNumSMs;
+    const int pref = (L->n_ot >= 3 || small) ? kModeStaged : kModeFused;
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
     for (int mode : modes) {
         if (force_mode >= 0 && mode != force_mode) continue;
@@ -152,14 +157,27 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                 if (S > 1 && min_buf == 1) continue;
                 for (int RT : kRTChoices) {
                     if (force_rt && RT != force_rt) continue;
-                    const ShapeRT sh = shape_rt(L->OT, RT);
+                    // warps per CTA: 16, or for batches too small to give every SM a
+                    // 16-warp CTA at RT = 4, the largest of {8, 4, 2, 1} that does
+                    int NW = kWarps;
+                    if (RT == kRTChoices[2] && S == 1 && mode != kModeGlobal) {
+                        const int force_nw = env_int("LMKAN_B200_NW", 0);
+                        if (force_nw) {
+                            NW = force_nw;
+                        } else {
+                            while (NW > 1 && ((rows + shape_rt(L->OT, RT, NW).R - 1) / shape_rt(L->OT, RT, NW).R) *
+                                                     L->n_ot < kNumSMs)
+                                NW >>= 1;
+                        }
+                    }
+                    const ShapeRT sh = shape_rt(L->OT, RT, NW);
                     const int64_t tiles = (rows + sh.R - 1) / sh.R;
                     if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
                     for (int nbuf = smem_sheet ? 4 : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
-                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S);
+                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW);
                         if (static_cast<int>(s.total) > smem_cap) continue;
                         out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, tiles, tiles * sh.R,
                                    mode == kModeStaged ? 2 : 1};
@@ -217,7 +235,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
         const int64_t py = (L->pairs + 15) / 16;
-        const int64_t gx = std::min<int64_t>(pl.rows_pad / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
+        const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
         records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
@@ -635,7 +653,7 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i
 }
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
-                    int* rows_per_cta_out, int* launches, int* mode, int* slabs) {
+                    int* rows_per_cta_out, int* launches, int* mode, int* slabs, int* warps_per_cta) {
     if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits");
@@ -646,6 +664,7 @@ int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int*
     if (launches) *launches = pl.launches;
     if (mode) *mode = pl.mode;
     if (slabs) *slabs = pl.S;
+    if (warps_per_cta) *warps_per_cta = pl.mode == kModeNarrow ? kNarrowThreads / 32 : pl.sh.NW;
     return LMKAN_B200_OK;
 }
 

@@ -275,6 +275,35 @@ def test_kernel_variants_parity_and_bitwise_agreement(torch, pkg, oracle, monkey
         assert torch.equal(Y, base), name
 
 
+@pytest.mark.parametrize("ot", ["64", "16"])
+def test_small_batch_warps_per_cta(torch, pkg, oracle, monkeypatch, ot):
+    """Small batches run CTAs of 8/4/2/1 warps (RT = 4) so the grid spans the
+    GPU; every warps-per-CTA choice meets the parity bar and is bitwise equal
+    to the 16-warp launch (the per-row summation order does not change)."""
+    n_in, n_out, G, rows = 64, 64, 8, 1024  # config 1
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=77)
+    Xd = torch.from_numpy(X).cuda()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 1.0)
+    monkeypatch.setenv("LMKAN_B200_OT", ot)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    auto = layer.plan(rows)
+    ctas = -(-rows // auto["rows_per_cta"]) * -(-n_out // auto["out_tile"])
+    assert auto["warps_per_cta"] < 16 and (ctas >= 148 or auto["warps_per_cta"] == 1), auto
+    outs = []
+    for mode in ("fused", "staged"):
+        monkeypatch.setenv("LMKAN_B200_MODE", mode)
+        for nw in ("16", "8", "4", "2", "1"):
+            monkeypatch.setenv("LMKAN_B200_NW", nw)
+            monkeypatch.setenv("LMKAN_B200_RT", "4")
+            plan = layer.plan(rows)
+            assert plan["warps_per_cta"] == int(nw) and plan["mode"] == mode, plan
+            Y = layer.forward(Xd)
+            assert _mixed(Y.cpu().numpy(), ref).max() <= TOL, (mode, nw)
+            outs.append(((mode, nw), Y))
+    for name, Y in outs[1:]:
+        assert torch.equal(Y, outs[0][1]), name
+
+
 def test_staged_row_chunking_bitwise(torch, pkg, monkeypatch):
     """Batches whose cell-record scratch exceeds the cap run in row chunks;
     results are bitwise identical to the unchunked launch."""

@@ -12,20 +12,35 @@ import paper_2509_07103_b200 as pkg  # noqa: E402
 
 
 def time_layer(layers, X, acts, iters=10):
+    """Device time per step; with SWEEP_GRAPH=1 the steps are captured in one
+    CUDA graph (no host launch gaps: the kernels' own time for tiny batches)."""
+    graph = os.environ.get("SWEEP_GRAPH") == "1"
     s = torch.cuda.current_stream()
 
     def step():
+        st = torch.cuda.current_stream()
         cur = X
         for lay, out in zip(layers, acts):
-            lay.forward_into(cur, out, s)
+            lay.forward_into(cur, out, st)
             cur = out
     for _ in range(3):
         step()
+    torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(iters):
+                step()
+        g.replay()
+        torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     a.record(s)
-    for _ in range(iters):
-        step()
+    if graph:
+        g.replay()
+    else:
+        for _ in range(iters):
+            step()
     b.record(s)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters
@@ -34,7 +49,10 @@ def time_layer(layers, X, acts, iters=10):
 def main():
     cfgn = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     cfg = bench.CONFIGS[cfgn]
-    variants = json.loads(os.environ.get("SWEEP", "[]")) or [
+    sw = os.environ.get("SWEEP", "[]")
+    if sw.endswith(".json"):
+        sw = open(sw).read()
+    variants = json.loads(sw) or [
         {"LMKAN_B200_MODE": m, "LMKAN_B200_RT": rt, "LMKAN_B200_NBUF": nb}
         for m in ("staged", "fused") for rt in ("16", "8") for nb in ("2", "1", "3")]
     G, B = cfg["G"], cfg["batch"]
@@ -42,7 +60,7 @@ def main():
     acts = [torch.empty((B, o), device="cuda") for _, o in cfg["layers"]]
     ot_cache = {}
     for v in variants:
-        for k in ("LMKAN_B200_MODE", "LMKAN_B200_RT", "LMKAN_B200_NBUF", "LMKAN_B200_OT"):
+        for k in [k for k in os.environ if k.startswith("LMKAN_B200_")]:
             os.environ.pop(k, None)
         os.environ.update(v)
         key = v.get("LMKAN_B200_OT", "")
