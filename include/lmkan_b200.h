@@ -34,8 +34,11 @@ extern "C" {
 #define LMKAN_B200_ECUDA 2   /* CUDA runtime / launch failure */
 #define LMKAN_B200_ENOMEM 3  /* device or pinned-host allocation failed */
 #define LMKAN_B200_ENOSYS 4  /* no sm_100a device / kernel image */
+#define LMKAN_B200_EFORMAT 5 /* malformed / truncated LMK1 file: lmkan::FormatError (errors.hpp:23-26) */
+#define LMKAN_B200_EUNSUPPORTED 6 /* valid LMK1 model with blocks outside the B200 path (mlp, bn, preconditioned) */
 
 typedef struct lmkan_b200_layer lmkan_b200_layer; /* opaque prepared device layer */
+typedef struct lmkan_b200_model lmkan_b200_model; /* opaque chain of device layers (a fused model) */
 
 /* Thread-local message for the last failing call on this thread. */
 const char* lmkan_b200_last_error(void);
@@ -159,6 +162,58 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, in
  * creation). Any output pointer may be NULL. */
 int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
                     int* nbuf, int* rows_per_cta, int* launches, int* mode, int* slabs, int* warps_per_cta);
+
+/* ---- models: the LMK1 container and the pure-lookup inference chain ----
+ *
+ * load_model (serialize.hpp:185-301) reads "LMK1" | u32 LE header length |
+ * JSON header | raw LE tensors, P in [i1][i2][pair][out] order, f64 or f32.
+ * model_infer (model.hpp:268-315) of a FUSED model (fuse_model,
+ * fuse.hpp:105-140: every block a pure lookup layer — type "lmkan", mode
+ * "none", no batch norm) is a chain of lmkan_forward calls; that chain is
+ * what the B200 model object runs. */
+
+/* load_model's validation without loading tensors (host only, no GPU): magic,
+ * header JSON, format/version, dtype, block metadata, manifest order and byte
+ * counts, truncated payload, trailing bytes — the same checks, in the same
+ * order, with the same lmkan::FormatError messages (EFORMAT). pure_lookup = 1
+ * when every block is a fused lookup block. Any output may be NULL. */
+int lmkan_b200_lmk1_inspect(const char* path, int* n_blocks, int* dtype_bytes, int* pure_lookup);
+/* Header metadata of one block: type 0 = lmkan, 1 = mlp, 2 = bn; mode 0 =
+ * relu_first, 1 = relu_last, 2 = linear, 3 = none (model.hpp:27-43);
+ * p_offset = byte offset of the block's P tensor in the file (lmkan blocks). */
+int lmkan_b200_lmk1_block(const char* path, int block, int* type, int* n_in, int* n_out, int* G,
+                          double* gamma, int* mode, int* has_bn, uint64_t* p_offset);
+/* One lmkan block's table straight from the file to a device layer (outputs
+ * [out_begin, out_end); out_end < 0 = all): streamed in 64 MB chunks through
+ * pinned buffers, rounded to fp32 and re-laid out on the device. The sharded
+ * loader for layers too wide for one GPU (config 5). */
+int lmkan_b200_layer_load_lmk1(const char* path, int block, int out_begin, int out_end, int device,
+                               lmkan_b200_layer** out);
+/* load_model of a fused model onto `device`: EFORMAT as load_model throws
+ * FormatError, EUNSUPPORTED if any block is not a pure lookup block. */
+int lmkan_b200_model_load(const char* path, int device, lmkan_b200_model** out);
+/* A chain over existing layers (borrowed: they must outlive the model). */
+int lmkan_b200_model_create(lmkan_b200_layer* const* layers, int n_layers, lmkan_b200_model** out);
+int lmkan_b200_model_info(const lmkan_b200_model* model, int* n_blocks, int* in_dim, int* out_dim,
+                          int* device);
+/* Borrowed pointer to block `block`'s layer (owned by the model). */
+int lmkan_b200_model_layer(const lmkan_b200_model* model, int block, lmkan_b200_layer** layer);
+/* model_infer on the device: X_dev [rows][in_dim] -> Y_dev [rows][out_dim],
+ * intermediate activations kept in device buffers owned by the model. The
+ * first call for a (rows, X, Y, stream) runs eagerly and captures a CUDA graph
+ * of the chain that later calls replay (not on the legacy NULL stream;
+ * LMKAN_B200_GRAPH=0 disables). Width mismatches between blocks fail with
+ * precond_forward's message (model.hpp:59). Calls on one model serialize. */
+int lmkan_b200_model_infer_f32(lmkan_b200_model* model, const float* X_dev, float* Y_dev, int64_t rows,
+                               void* stream);
+int lmkan_b200_model_infer_f64(lmkan_b200_model* model, const double* X_dev, double* Y_dev,
+                               int64_t rows, void* stream);
+/* Drop-in synchronous model_infer with host X/Y; `workers` ignored. */
+int lmkan_b200_model_infer_host_f64(lmkan_b200_model* model, const double* X, double* Y, int64_t rows,
+                                    size_t workers);
+int lmkan_b200_model_infer_host_f32(lmkan_b200_model* model, const float* X, float* Y, int64_t rows,
+                                    size_t workers);
+int lmkan_b200_model_destroy(lmkan_b200_model* model);
 
 #ifdef __cplusplus
 }

@@ -24,9 +24,11 @@ from typing import Optional, Tuple
 
 import numpy as np
 
-from ._lib import LIB_PATH, LmkanError, check, lib  # noqa: F401  (fails loudly if the .so is missing)
+from ._lib import LIB_PATH, FormatError, LmkanError, UnsupportedModelError, check, lib  # noqa: F401  (fails loudly if the .so is missing)
 
 __all__ = ["SigmaGrid", "build_grid", "thresholds", "init_table", "Layer", "LmKanLayer", "init_layer",
+           "Model", "load_model", "model_infer", "lmk1_inspect", "lmk1_block", "FormatError",
+           "UnsupportedModelError",
            "lmkan_forward", "LmkanError", "LIB_PATH", "version"]
 
 
@@ -91,8 +93,9 @@ class Layer:
     """Prepared device layer (opaque ``lmkan_b200_layer*``): fp32 table in the
     [out_tile][pair][node][OT] layout, grid constants and locate thresholds."""
 
-    def __init__(self, handle: C.c_void_p):
+    def __init__(self, handle: C.c_void_p, owned: bool = True):
         self._h = handle
+        self._owned = owned  # False for layers borrowed from a Model
         n_in, n_out, G, dev, ot = (C.c_int() for _ in range(5))
         tb = C.c_size_t()
         check(lib.lmkan_b200_layer_info(self._h, C.byref(n_in), C.byref(n_out), C.byref(G), C.byref(dev),
@@ -137,6 +140,17 @@ class Layer:
         h = C.c_void_p()
         check(lib.lmkan_b200_layer_create_random(int(n_in), int(n_out), int(G), float(gamma), int(seed),
                                                  float(scale), int(ob), int(oe), int(device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_lmk1(cls, path: str, block: int = 0, out_range: Optional[Tuple[int, int]] = None,
+                  device: int = 0) -> "Layer":
+        """One lmkan block of an LMK1 file straight to the device (optionally an
+        output slice [ob, oe)): the table is streamed from disk in chunks."""
+        ob, oe = out_range if out_range else (0, -1)
+        h = C.c_void_p()
+        check(lib.lmkan_b200_layer_load_lmk1(str(path).encode(), int(block), int(ob), int(oe), int(device),
+                                             C.byref(h)))
         return cls(h)
 
     # -- forward ------------------------------------------------------------
@@ -229,7 +243,8 @@ class Layer:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            lib.lmkan_b200_layer_destroy(self._h)
+            if getattr(self, "_owned", True):
+                lib.lmkan_b200_layer_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -237,6 +252,113 @@ class Layer:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# Models: the LMK1 container (serialize.hpp:185-301) and model_infer of a fused
+# pure-lookup model (model.hpp:268-315, fuse.hpp:105-140) as one device chain.
+
+_BLOCK_TYPES = {0: "lmkan", 1: "mlp", 2: "bn"}
+_MODES = {0: "relu_first", 1: "relu_last", 2: "linear", 3: "none"}
+
+
+def lmk1_inspect(path: str) -> dict:
+    """load_model's validation only (host, no GPU); raises FormatError /
+    ValueError exactly where load_model throws FormatError / invalid_argument."""
+    nb, elem, pure = C.c_int(), C.c_int(), C.c_int()
+    check(lib.lmkan_b200_lmk1_inspect(str(path).encode(), C.byref(nb), C.byref(elem), C.byref(pure)))
+    return {"blocks": nb.value, "dtype": "f32" if elem.value == 4 else "f64", "pure_lookup": bool(pure.value)}
+
+
+def lmk1_block(path: str, block: int) -> dict:
+    t, n_in, n_out, G, mode, bn = (C.c_int() for _ in range(6))
+    gamma, off = C.c_double(), C.c_uint64()
+    check(lib.lmkan_b200_lmk1_block(str(path).encode(), int(block), C.byref(t), C.byref(n_in), C.byref(n_out),
+                                    C.byref(G), C.byref(gamma), C.byref(mode), C.byref(bn), C.byref(off)))
+    return {"type": _BLOCK_TYPES[t.value], "n_in": n_in.value, "n_out": n_out.value, "G": G.value,
+            "gamma": gamma.value, "mode": _MODES[mode.value], "bn": bool(bn.value), "p_offset": off.value}
+
+
+class Model:
+    """Opaque ``lmkan_b200_model*``: a chain of device layers (a fused model)."""
+
+    def __init__(self, handle: C.c_void_p, keep=None):
+        self._h = handle
+        self._keep = keep  # borrowed layers must outlive the model
+        nb, di, do, dev = (C.c_int() for _ in range(4))
+        check(lib.lmkan_b200_model_info(self._h, C.byref(nb), C.byref(di), C.byref(do), C.byref(dev)))
+        self.n_blocks, self.in_dim, self.out_dim, self.device = nb.value, di.value, do.value, dev.value
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "Model":
+        h = C.c_void_p()
+        check(lib.lmkan_b200_model_load(str(path).encode(), int(device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_layers(cls, layers) -> "Model":
+        arr = (C.c_void_p * len(layers))(*[lay._h for lay in layers])
+        h = C.c_void_p()
+        check(lib.lmkan_b200_model_create(arr, len(layers), C.byref(h)))
+        return cls(h, keep=list(layers))
+
+    def layer(self, block: int) -> Layer:
+        h = C.c_void_p()
+        check(lib.lmkan_b200_model_layer(self._h, int(block), C.byref(h)))
+        lay = Layer(h, owned=False)
+        lay._model = self  # keep the owner alive
+        return lay
+
+    def infer_into(self, X, Y, stream=None) -> None:
+        """Device path (CUDA graph replay after the first call per shape/stream)."""
+        import torch
+        if X.dim() != 2 or X.shape[1] != self.in_dim:
+            raise ValueError(f"precond_forward: expected width {self.in_dim}, got {X.shape[-1]}")
+        assert X.is_cuda and Y.is_cuda and X.is_contiguous() and Y.is_contiguous() and X.dtype == Y.dtype
+        assert Y.shape == (X.shape[0], self.out_dim)
+        fn = lib.lmkan_b200_model_infer_f32 if X.dtype == torch.float32 else lib.lmkan_b200_model_infer_f64
+        check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream)))
+
+    def infer(self, X, stream=None):
+        if isinstance(X, np.ndarray):
+            return self.infer_host(X)
+        import torch
+        Y = torch.empty((X.shape[0], self.out_dim), dtype=X.dtype, device=X.device)
+        self.infer_into(X, Y, stream)
+        return Y
+
+    def infer_host(self, X: np.ndarray) -> np.ndarray:
+        X = np.asarray(X)
+        if X.ndim != 2 or X.shape[1] != self.in_dim:
+            raise ValueError(f"precond_forward: expected width {self.in_dim}, got {X.shape[-1]}")
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        Y = np.empty((X.shape[0], self.out_dim), X.dtype)
+        fn = lib.lmkan_b200_model_infer_host_f32 if X.dtype == np.float32 else lib.lmkan_b200_model_infer_host_f64
+        check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), 0))
+        return Y
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.lmkan_b200_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def load_model(path: str, device: int = 0) -> Model:
+    """serialize.hpp:185-301 for fused pure-lookup models, onto `device`."""
+    return Model.load(path, device)
+
+
+def model_infer(model: Model, X: np.ndarray, workers: int = 0) -> np.ndarray:
+    """model.hpp:313-316: host X [rows, in_dim] -> host Y; `workers` ignored."""
+    return model.infer_host(np.ascontiguousarray(X, np.float64))
 
 
 # ---------------------------------------------------------------------------

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "liblmkan_b200.so")
 
-OK, EINVAL, ECUDA, ENOMEM, ENOSYS = 0, 1, 2, 3, 4
+OK, EINVAL, ECUDA, ENOMEM, ENOSYS, EFORMAT, EUNSUPPORTED = 0, 1, 2, 3, 4, 5, 6
 
 # (name, restype, argtypes) — must match include/lmkan_b200.h exactly;
 # tests/test_capi.py checks every declared symbol is exported.
@@ -45,6 +45,18 @@ _SIGS = [
     ("lmkan_b200_locate_f32", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),
     ("lmkan_b200_locate_f64", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),
     ("lmkan_b200_plan", C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("lmkan_b200_lmk1_inspect", C.c_int, [C.c_char_p, _P, _P, _P]),
+    ("lmkan_b200_lmk1_block", C.c_int, [C.c_char_p, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("lmkan_b200_layer_load_lmk1", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_model_load", C.c_int, [C.c_char_p, C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_model_create", C.c_int, [C.POINTER(_P), C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_model_info", C.c_int, [_P, _P, _P, _P, _P]),
+    ("lmkan_b200_model_layer", C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_model_infer_f32", C.c_int, [_P, _P, _P, C.c_int64, _P]),
+    ("lmkan_b200_model_infer_f64", C.c_int, [_P, _P, _P, C.c_int64, _P]),
+    ("lmkan_b200_model_infer_host_f64", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
+    ("lmkan_b200_model_infer_host_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
+    ("lmkan_b200_model_destroy", C.c_int, [_P]),
 ]
 
 
@@ -68,6 +80,15 @@ class LmkanError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+        self.msg = msg
+
+
+class FormatError(LmkanError):
+    """lmkan::FormatError (errors.hpp:23-26): malformed or truncated LMK1 file."""
+
+
+class UnsupportedModelError(LmkanError):
+    """A valid LMK1 model with blocks outside the B200 path (mlp / bn / preconditioned)."""
 
 
 def check(rc: int) -> None:
@@ -76,4 +97,8 @@ def check(rc: int) -> None:
         if rc == EINVAL:
             # the reference raises std::invalid_argument for the same conditions
             raise ValueError(msg)
+        if rc == EFORMAT:
+            raise FormatError(rc, msg)
+        if rc == EUNSUPPORTED:
+            raise UnsupportedModelError(rc, msg)
         raise LmkanError(rc, msg)

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -35,5 +36,18 @@ struct Plan {
 template <int OT, typename XT>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
                           const float4* recW, const int* recO, const InputMap& im, cudaStream_t st);
+
+// Entry points shared with the other host translation units (model.cu):
+// defined in lmkan_b200.cu next to the layer C-ABI.
+namespace api {
+int set_error(int code, const std::string& msg);  // thread-local lmkan_b200_last_error
+int cuda_error(cudaError_t e, const char* what);  // maps a CUDA error to a status code
+// Handle + grid constants + (uninitialised) device table for outputs
+// [out_begin, out_begin + n_out_local) of an n_out_total-wide layer.
+int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,
+                lmkan_b200_layer** out);
+int forward_device(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, cudaStream_t st);
+int forward_device(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st);
+}  // namespace api
 
 }  // namespace lmkan_b200

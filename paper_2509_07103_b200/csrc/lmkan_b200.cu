@@ -460,6 +460,21 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
 
 }  // namespace
 
+namespace lmkan_b200::api {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+int cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,
+                lmkan_b200_layer** out) {
+    return ::alloc_layer(n_in, n_out_local, n_out_total, out_begin, G, gamma, device, out);
+}
+int forward_device(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, cudaStream_t st) {
+    return ::forward_device<float>(L, X, Y, rows, st);
+}
+int forward_device(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st) {
+    return ::forward_device<double>(L, X, Y, rows, st);
+}
+}  // namespace lmkan_b200::api
+
 // =================================================================== C-ABI
 extern "C" {
 
