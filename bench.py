@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    1: dict(name="cfg1: lmKAN layer 64->64, G=8, batch 1024", layers=[(64, 64)], G=8, batch=1024),
+    1: dict(name="cfg1: lmKAN layer 64->64, G=8, batch 1024", layers=[(64, 64)], G=8, batch=1024, small=True),
     2: dict(name="cfg2: lmKAN layer 1024->1024, G=16, batch 65536", layers=[(1024, 1024)], G=16, batch=65536),
     3: dict(name="cfg3: methane pure-lookup chain 12->128->128->1, G=28, batch 1048576",
             layers=[(12, 128), (128, 128), (128, 1)], G=28, batch=1 << 20),
@@ -270,7 +270,12 @@ def main():
     else:
         X = torch.randn((B, cfg["layers"][0][0]), generator=gen, device=f"cuda:{local}", dtype=torch.float32)
     acts = [torch.empty((B, n_out), device=f"cuda:{local}", dtype=torch.float32) for _, n_out in cfg["layers"]]
-    stream = torch.cuda.current_stream()
+    # Chains (and launch-bound tiny batches) run through the model API: one
+    # device chain per step, replayed from a CUDA graph (needs a non-legacy
+    # stream); single wide layers launch directly on the current stream.
+    use_model = not conv and not out_sharded and (len(layers) > 1 or bool(cfg.get("small")))
+    model = pkg.Model.from_layers(layers) if use_model else None
+    stream = torch.cuda.Stream() if use_model else torch.cuda.current_stream()
     K = args.steps
     # gather-kernel events per step and layer (the dominant kernel, timed alone
     # through lmkan_b200_forward_f32_timed); created by one record each
@@ -281,8 +286,11 @@ def main():
             a.record(stream)
             b.record(stream)
 
-    def step(i=None, src=None):
+    def step(i=None, src=None, eager=False):
         cur = X if src is None else src
+        if model is not None and not eager:
+            model.infer_into(cur, acts[-1], stream)
+            return
         for li, (lay, out) in enumerate(zip(layers, acts)):
             if conv and li == 0:
                 if i is not None:
@@ -312,11 +320,17 @@ def main():
         sampler.begin()
     start.record(stream)
     for i in range(K):
-        step(i)
+        step(None if model is not None else i)
     stop.record(stream)
     torch.cuda.synchronize()
     if sampler:
         sampler.end()
+    if model is not None:
+        # graph replays carry no per-kernel events: time the gather kernels in
+        # an eager pass of the same K steps right after the timed region
+        for i in range(K):
+            step(i, eager=True)
+        torch.cuda.synchronize()
     if dist:
         dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
@@ -345,7 +359,9 @@ def main():
         single = len(layers) == 1 and not conv
 
         def host_step():
-            if single:
+            if model is not None:  # model_infer drop-in: chunked H2D / graph chain / D2H
+                model.infer_host_ptr(Xh.data_ptr(), Yh.data_ptr(), B, np.float32)
+            elif single:
                 layers[0].forward_host_ptr(Xh.data_ptr(), Yh.data_ptr(), B, np.float32)
             else:
                 Xd = torch.empty_like(X)
@@ -426,6 +442,10 @@ def main():
                      "kernel_share_of_step": kernel_ms / ms_per_step,
                      "note": "B_alg = 8*n_in*n_out + 4*(n_in+n_out) per row (gather-from-HBM model); "
                              "frac > 1 means table reuse from SMEM/L2",
+                     "kernel_timing": ("CUDA events around each gather kernel on the launch stream, eager pass of "
+                                       "the same K steps after the graph-replayed timed region")
+                     if model is not None else
+                     "CUDA events around each gather kernel on the launch stream, inside the timed region",
                      "fp32_fma_tflops": fmas / (kernel_ms / 1e3) / 1e12},
         "clocks": clocks,
         "e2e": e2e,

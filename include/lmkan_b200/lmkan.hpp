@@ -8,6 +8,9 @@
 //   LmKanLayer                      layer.hpp:24-61 (same fields and P layout)
 //   default_init_scale, init_layer  layer.hpp:63-86 (bit-identical table)
 //   lmkan_forward                   layer.hpp:108-134 (same signature)
+//   FormatError                     errors.hpp:23-26
+//   load_model, model_infer         serialize.hpp:185-301, model.hpp:313-316,
+//                                   for fused pure-lookup models (DeviceModel)
 // Existing callers switch with `namespace lmkan = lmkan_b200;` (see
 // INTEGRATION.md). Errors: std::invalid_argument where the reference throws it
 // (same messages), std::runtime_error for CUDA failures. There is no CPU
@@ -32,11 +35,17 @@
 
 namespace lmkan_b200 {
 
+// errors.hpp:23-26: malformed or truncated model file.
+struct FormatError : std::runtime_error {
+    explicit FormatError(const std::string& msg) : std::runtime_error(msg) {}
+};
+
 namespace detail {
 inline void throw_status(int rc, const char* where) {
     if (rc == LMKAN_B200_OK) return;
     const std::string msg = lmkan_b200_last_error();
     if (rc == LMKAN_B200_EINVAL) throw std::invalid_argument(msg);
+    if (rc == LMKAN_B200_EFORMAT) throw FormatError(msg);
     throw std::runtime_error(std::string(where) + ": " + msg);
 }
 }  // namespace detail
@@ -231,6 +240,47 @@ inline void lmkan_forward(const LmKanLayer& layer, const Matrix& X, Matrix& Y, s
     detail::throw_status(lmkan_b200_forward_host_f64(h, X.data(), Y.data(), static_cast<std::int64_t>(X.rows()),
                                                      workers),
                          "lmkan_forward");
+}
+
+// A fused pure-lookup model resident on one GPU: what load_model returns for a
+// model that went through fuse_model (fuse.hpp:105-140), as a chain of device
+// layers. Blocks of other kinds (mlp, batch norm, preconditioned lookup) are
+// outside the B200 path: load_model throws std::runtime_error for them.
+class DeviceModel {
+public:
+    DeviceModel() = default;
+    explicit DeviceModel(lmkan_b200_model* h) : h_(h, &lmkan_b200_model_destroy) {
+        detail::throw_status(lmkan_b200_model_info(h, &n_blocks_, &in_dim_, &out_dim_, &device_), "load_model");
+    }
+    int in_dim() const { return in_dim_; }
+    int out_dim() const { return out_dim_; }
+    int n_blocks() const { return n_blocks_; }
+    int device() const { return device_; }
+    lmkan_b200_model* handle() const { return h_.get(); }
+
+private:
+    std::shared_ptr<lmkan_b200_model> h_;
+    int n_blocks_ = 0, in_dim_ = 0, out_dim_ = 0, device_ = 0;
+};
+
+// serialize.hpp:185-301: same validation and FormatError messages; the tables
+// are streamed from the file straight into the device layout.
+inline DeviceModel load_model(const std::string& path, int device = 0) {
+    lmkan_b200_model* h = nullptr;
+    detail::throw_status(lmkan_b200_model_load(path.c_str(), device, &h), "load_model");
+    return DeviceModel(h);
+}
+
+// model.hpp:313-316 (inference forward). Width errors as precond_forward's
+// require_width (model.hpp:59). `workers` is accepted and ignored.
+inline Matrix model_infer(const DeviceModel& model, const Matrix& X, std::size_t workers = 0) {
+    require_width(X, static_cast<std::size_t>(model.in_dim()), "precond_forward");
+    Matrix Y(X.rows(), model.out_dim());
+    if (X.rows() == 0) return Y;
+    detail::throw_status(lmkan_b200_model_infer_host_f64(model.handle(), X.data(), Y.data(),
+                                                         static_cast<std::int64_t>(X.rows()), workers),
+                         "model_infer");
+    return Y;
 }
 
 // Adapter for code that keeps the REFERENCE's own types (lmkan::LmKanLayer,

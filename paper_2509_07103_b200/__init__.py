@@ -339,6 +339,10 @@ class Model:
         check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), 0))
         return Y
 
+    def infer_host_ptr(self, X_ptr: int, Y_ptr: int, rows: int, dtype=np.float32) -> None:
+        fn = lib.lmkan_b200_model_infer_host_f32 if dtype == np.float32 else lib.lmkan_b200_model_infer_host_f64
+        check(fn(self._h, C.c_void_p(X_ptr), C.c_void_p(Y_ptr), int(rows), 0))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib.lmkan_b200_model_destroy(self._h)

@@ -369,24 +369,42 @@ struct lmkan_b200_model {
     std::vector<lmkan_b200_layer*> layers;
     bool owns = false;
     int device = 0;
-    std::mutex mu;
-    // intermediate activations (fp32 / fp64), reused across calls
-    void* acts[2] = {nullptr, nullptr};
-    size_t act_bytes[2] = {0, 0};
+    std::mutex mu;       // device-path state below
+    std::mutex host_mu;  // host-path staging
+    // Per-stream ping-pong buffers for the intermediate activations, so chains
+    // in flight on different streams never share them.
+    struct StreamActs {
+        cudaStream_t st;
+        void* acts[2];
+        size_t bytes;
+    };
+    std::vector<StreamActs> acts;
     struct GraphEntry {
         int64_t rows;
+        int elem;  // sizeof(XT): f32 and f64 chains on the same buffers are different graphs
         const void* X;
         void* Y;
         cudaStream_t st;
         cudaGraphExec_t exec;
     };
     std::list<GraphEntry> graphs;  // most recent first, at most kMaxGraphs
-    static constexpr size_t kMaxGraphs = 4;
+    static constexpr size_t kMaxGraphs = 6;
+    // host path: two streams, device X/Y staging per stream
+    cudaStream_t hst[2] = {nullptr, nullptr};
+    void* hX[2] = {nullptr, nullptr};
+    void* hY[2] = {nullptr, nullptr};
+    size_t hX_bytes = 0, hY_bytes = 0;
 
     ~lmkan_b200_model() {
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
-        for (void* a : acts)
-            if (a) cudaFree(a);
+        for (auto& a : acts)
+            for (void* p : a.acts)
+                if (p) cudaFree(p);
+        for (int i = 0; i < 2; ++i) {
+            if (hX[i]) cudaFree(hX[i]);
+            if (hY[i]) cudaFree(hY[i]);
+            if (hst[i]) cudaStreamDestroy(hst[i]);
+        }
         if (owns)
             for (auto* L : layers) lmkan_b200_layer_destroy(L);
     }
@@ -412,38 +430,56 @@ int check_chain(const lmkan_b200_model* M) {
     return LMKAN_B200_OK;
 }
 
-// Ping-pong activation buffers big enough for `rows` rows of every
-// intermediate width.
-int ensure_acts(lmkan_b200_model* M, int64_t rows, size_t elem) {
+// Ping-pong activation buffers of stream `st`, big enough for `rows` rows of
+// every intermediate width. Growing them drops the graphs captured on `st`.
+int ensure_acts(lmkan_b200_model* M, int64_t rows, size_t elem, cudaStream_t st, void** out) {
     size_t need = 0;
     for (size_t b = 0; b + 1 < M->layers.size(); ++b) {
         int n_out = 0;
         layer_width(M->layers[b], nullptr, &n_out);
         need = std::max(need, static_cast<size_t>(rows) * n_out * elem);
     }
-    for (int i = 0; i < 2; ++i) {
-        if (M->act_bytes[i] >= need) continue;
-        if (M->acts[i]) {
-            cudaDeviceSynchronize();  // graphs captured with the old buffer must not run again
-            cudaFree(M->acts[i]);
-            M->acts[i] = nullptr;
-            M->act_bytes[i] = 0;
-            for (auto& g : M->graphs) cudaGraphExecDestroy(g.exec);
-            M->graphs.clear();
-        }
-        cudaError_t e = cudaMalloc(&M->acts[i], need);
-        if (e != cudaSuccess) return api::cuda_error(e, "model_infer: activation buffers");
-        M->act_bytes[i] = need;
+    lmkan_b200_model::StreamActs* sa = nullptr;
+    for (auto& a : M->acts)
+        if (a.st == st) sa = &a;
+    if (!sa) {
+        M->acts.push_back({st, {nullptr, nullptr}, 0});
+        sa = &M->acts.back();
     }
+    if (sa->bytes < need) {
+        if (sa->acts[0] || sa->acts[1]) {
+            cudaStreamSynchronize(st);  // work (and graphs) using the old buffers must be done
+            for (auto it = M->graphs.begin(); it != M->graphs.end();) {
+                if (it->st == st) {
+                    cudaGraphExecDestroy(it->exec);
+                    it = M->graphs.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+            for (void*& p : sa->acts) {
+                if (p) cudaFree(p);
+                p = nullptr;
+            }
+            sa->bytes = 0;
+        }
+        for (void*& p : sa->acts) {
+            cudaError_t e = cudaMalloc(&p, need);
+            if (e != cudaSuccess) return api::cuda_error(e, "model_infer: activation buffers");
+        }
+        sa->bytes = need;
+    }
+    out[0] = sa->acts[0];
+    out[1] = sa->acts[1];
     return LMKAN_B200_OK;
 }
 
 template <typename XT>
-int run_chain(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+int run_chain(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStream_t st, void* const* acts) {
     const XT* cur = X;
     const size_t n = M->layers.size();
     for (size_t b = 0; b < n; ++b) {
-        XT* dst = b + 1 == n ? Y : static_cast<XT*>(M->acts[b & 1]);
+        XT* dst = b + 1 == n ? Y : static_cast<XT*>(acts[b & 1]);
         if (int rc = api::forward_device(M->layers[b], cur, dst, rows, st)) return rc;
         cur = dst;
     }
@@ -473,7 +509,8 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
             if (d != cur) cudaSetDevice(d);
         }
     } restore{dev_prev, M->device};
-    if (int rc = ensure_acts(M, rows, sizeof(XT))) return rc;
+    void* acts[2];
+    if (int rc = ensure_acts(M, rows, sizeof(XT), st, acts)) return rc;
     // graph replay for a (rows, X, Y, stream) seen before (not on the legacy
     // stream, which cannot be captured, nor while the caller is capturing)
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -481,7 +518,8 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
                            cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
     if (graphable) {
         for (auto it = M->graphs.begin(); it != M->graphs.end(); ++it) {
-            if (it->rows == rows && it->X == X && it->Y == Y && it->st == st) {
+            if (it->rows == rows && it->elem == static_cast<int>(sizeof(XT)) && it->X == X && it->Y == Y &&
+                it->st == st) {
                 M->graphs.splice(M->graphs.begin(), M->graphs, it);
                 cudaError_t e = cudaGraphLaunch(M->graphs.front().exec, st);
                 if (e != cudaSuccess) return api::cuda_error(e, "model_infer: graph launch");
@@ -490,19 +528,19 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
         }
     }
     // first sight: run eagerly (validates every launch), then capture
-    if (int rc = run_chain<XT>(M, X, Y, rows, st)) return rc;
+    if (int rc = run_chain<XT>(M, X, Y, rows, st, acts)) return rc;
     if (!graphable) return LMKAN_B200_OK;
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
         return LMKAN_B200_OK;
     }
-    const int rc = run_chain<XT>(M, X, Y, rows, st);
+    const int rc = run_chain<XT>(M, X, Y, rows, st, acts);
     const cudaError_t e_end = cudaStreamEndCapture(st, &g);
     cudaGraphExec_t exec = nullptr;
     if (rc == LMKAN_B200_OK && e_end == cudaSuccess && g &&
         cudaGraphInstantiateWithFlags(&exec, g, cudaGraphInstantiateFlagAutoFreeOnLaunch) == cudaSuccess) {
-        M->graphs.push_front({rows, X, Y, st, exec});
+        M->graphs.push_front({rows, static_cast<int>(sizeof(XT)), X, Y, st, exec});
         if (M->graphs.size() > lmkan_b200_model::kMaxGraphs) {
             cudaGraphExecDestroy(M->graphs.back().exec);
             M->graphs.pop_back();
@@ -513,39 +551,71 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
     return LMKAN_B200_OK;
 }
 
+// Drop-in host path: rows in chunks alternating over two model-owned streams,
+// so the H2D of chunk c+1 and the D2H of chunk c-1 overlap the chain on chunk
+// c; each (chunk shape, stream) replays its own captured graph.
 template <typename XT>
 int infer_host(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows) {
     if (!M || M->layers.empty()) return api::set_error(LMKAN_B200_EINVAL, "model_infer: null or empty model");
     if (rows < 0) return api::set_error(LMKAN_B200_EINVAL, "model_infer: negative row count");
     if (rows == 0) return LMKAN_B200_OK;
     if (!X || !Y) return api::set_error(LMKAN_B200_EINVAL, "model_infer: null X or Y");
+    std::lock_guard<std::mutex> lock(M->host_mu);
     int n_in = 0, n_out = 0;
     layer_width(M->layers.front(), &n_in, nullptr);
     layer_width(M->layers.back(), nullptr, &n_out);
     int dev_prev = 0;
     cudaGetDevice(&dev_prev);
     if (dev_prev != M->device) cudaSetDevice(M->device);
-    cudaStream_t st = nullptr;
-    XT *dX = nullptr, *dY = nullptr;
+    struct Restore {
+        int d, cur;
+        ~Restore() {
+            if (d != cur) cudaSetDevice(d);
+        }
+    } restore{dev_prev, M->device};
+    const int64_t chunk = std::min<int64_t>(rows, std::max<int64_t>((rows + 3) / 4, 65536));
+    const size_t xb = sizeof(XT) * static_cast<size_t>(chunk) * n_in, yb = sizeof(XT) * static_cast<size_t>(chunk) * n_out;
+    for (int i = 0; i < 2; ++i) {
+        cudaError_t e = cudaSuccess;
+        if (!M->hst[i]) e = cudaStreamCreateWithFlags(&M->hst[i], cudaStreamNonBlocking);
+        if (e != cudaSuccess) return api::cuda_error(e, "model_infer: streams");
+    }
+    if (M->hX_bytes < xb || M->hY_bytes < yb) {
+        for (int i = 0; i < 2; ++i) {
+            cudaStreamSynchronize(M->hst[i]);
+            if (M->hX[i]) cudaFree(M->hX[i]);
+            if (M->hY[i]) cudaFree(M->hY[i]);
+            M->hX[i] = M->hY[i] = nullptr;
+        }
+        M->hX_bytes = M->hY_bytes = 0;
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = cudaMalloc(&M->hX[i], xb);
+            if (e == cudaSuccess) e = cudaMalloc(&M->hY[i], yb);
+            if (e != cudaSuccess) return api::cuda_error(e, "model_infer: host staging");
+        }
+        M->hX_bytes = xb;
+        M->hY_bytes = yb;
+    }
     int rc = LMKAN_B200_OK;
-    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dX), sizeof(XT) * rows * n_in, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dY), sizeof(XT) * rows * n_out, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dX, X, sizeof(XT) * rows * n_in, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) rc = api::cuda_error(e, "model_infer: host staging");
-    if (rc == LMKAN_B200_OK) rc = infer_device<XT>(M, dX, dY, rows, st);
-    if (rc == LMKAN_B200_OK) {
-        e = cudaMemcpyAsync(Y, dY, sizeof(XT) * rows * n_out, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    int c = 0;
+    for (int64_t r0 = 0; r0 < rows && rc == LMKAN_B200_OK; r0 += chunk, ++c) {
+        const int i = c & 1;
+        const int64_t n = std::min(chunk, rows - r0);
+        cudaStream_t st = M->hst[i];
+        cudaError_t e = cudaMemcpyAsync(M->hX[i], X + r0 * n_in, sizeof(XT) * n * n_in, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            rc = api::cuda_error(e, "model_infer: H2D");
+            break;
+        }
+        rc = infer_device<XT>(M, static_cast<const XT*>(M->hX[i]), static_cast<XT*>(M->hY[i]), n, st);
+        if (rc) break;
+        e = cudaMemcpyAsync(Y + r0 * n_out, M->hY[i], sizeof(XT) * n * n_out, cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) rc = api::cuda_error(e, "model_infer: D2H");
     }
-    if (dX) cudaFreeAsync(dX, st);
-    if (dY) cudaFreeAsync(dY, st);
-    if (st) {
-        cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
+    for (int i = 0; i < 2; ++i) {
+        const cudaError_t e = cudaStreamSynchronize(M->hst[i]);
+        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = api::cuda_error(e, "model_infer: stream sync");
     }
-    if (dev_prev != M->device) cudaSetDevice(dev_prev);
     return rc;
 }
 

@@ -6,8 +6,12 @@
 // fp32 contract |d| <= 1e-5 * max(1, |ref|) instead of the reference's fp64 1e-12.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
 #include <random>
 #include <stdexcept>
+#include <cstring>
+#include <string>
+#include <vector>
 
 #include "lmkan_b200/lmkan.hpp"
 
@@ -176,13 +180,69 @@ static void test_interval_index() {  // test_grid.cpp:108-114
     CHECK(interval_index(g4, std::nan("")) == 0);
 }
 
-int main() {
+// serialize.hpp:185-301 + model.hpp:313-316 on a model the REFERENCE saved
+// (tests/golden/lmk1/pure_f64.lmk1, fuse_model of a relu_first student):
+// model_infer equals the chain of lmkan_forward calls over layers built from
+// the file's own P tensors; corrupt files throw FormatError with load_model's
+// message; unfused models are refused.
+static void test_load_model(const std::string& gold) {
+    const std::string path = gold + "/pure_f64.lmk1";
+    const DeviceModel model = load_model(path);
+    CHECK(model.n_blocks() == 3 && model.in_dim() == 6 && model.out_dim() == 3);
+    std::ifstream in(path, std::ios::binary);
+    std::vector<char> raw((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::vector<LmKanLayer> layers;
+    for (int b = 0; b < 3; ++b) {
+        int type, n_in, n_out, G, mode, has_bn;
+        double gamma;
+        std::uint64_t off;
+        CHECK(lmkan_b200_lmk1_block(path.c_str(), b, &type, &n_in, &n_out, &G, &gamma, &mode, &has_bn, &off) == 0);
+        LmKanLayer L;
+        L.n_in = n_in;
+        L.n_out = n_out;
+        L.grid = build_grid(G);
+        L.gamma = gamma;
+        L.P.resize(static_cast<std::size_t>(G + 1) * (G + 1) * (n_in / 2) * n_out);
+        std::memcpy(L.P.data(), raw.data() + off, L.P.size() * sizeof(double));
+        layers.push_back(std::move(L));
+    }
+    std::mt19937_64 g(21);
+    const Matrix X = random_batch(40, 6, g, 1.5);
+    const Matrix Y = model_infer(model, X);
+    Matrix cur = X;
+    for (const LmKanLayer& L : layers) {
+        Matrix nxt;
+        lmkan_forward(L, cur, nxt);
+        cur = nxt;
+    }
+    CHECK(Y.rows() == 40 && Y.cols() == 3);
+    for (std::size_t i = 0; i < Y.size(); ++i) CHECK(close_mixed(Y.data()[i], cur.data()[i]));
+    Matrix bad(2, 5);
+    CHECK_THROWS_AS(model_infer(model, bad), std::invalid_argument);
+    // corrupt file: bad magic
+    const std::string tmp = "/tmp/lmkan_b200_bad_magic.lmk1";
+    {
+        std::ofstream o(tmp, std::ios::binary);
+        o.write("LMK2", 4);
+        o.write(raw.data() + 4, static_cast<std::streamsize>(raw.size() - 4));
+    }
+    try {
+        load_model(tmp);
+        CHECK(false);
+    } catch (const FormatError& e) {
+        CHECK(std::string(e.what()) == "load_model: bad magic, not an LMK1 model file");
+    }
+    CHECK_THROWS_AS(load_model(gold + "/student.lmk1"), std::runtime_error);
+}
+
+int main(int argc, char** argv) {
     test_init_layer();
     test_dense_oracle();
     test_width_mismatch();
     test_linear_sheets();
     test_determinism_and_cache();
     test_interval_index();
+    if (argc > 1) test_load_model(argv[1]);
     std::printf("test_dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }

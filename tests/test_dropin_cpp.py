@@ -15,7 +15,8 @@ def test_cpp_dropin_api():
     if not os.path.exists(BIN):
         import __graft_entry__ as g
         g.build_cpp_tests()
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden", "lmk1")], capture_output=True, text=True,
+                       timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
 
