@@ -34,6 +34,7 @@ struct GridConst {
     float t32[kMaxThr];   // thresholds, NaN-padded to L entries
     double t64[kMaxThr];
     double points[kMaxThr + 1];
+    double inv_h[kMaxThr];  // 1 / (points[i+1] - points[i]), the per-axis factors of inv_areas (grid.hpp:58-64)
     const double* inv_areas;  // device [G*G]
     int G;
     int L;  // power of two >= G (search width)
@@ -107,6 +108,18 @@ __device__ __forceinline__ float4 lds128_if(const void* p, bool pred) {
         "mov.f32 %2, 0f00000000;\n\tmov.f32 %3, 0f00000000;\n\t"
         "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(smem_addr(p)), "r"(static_cast<int>(pred))
+        : "memory");
+    return v;
+}
+__device__ __forceinline__ float2 lds64_if(const void* p, bool pred) {
+    float2 v;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.b32 q, %3, 0;\n\t"
+        "mov.f32 %0, 0f00000000;\n\tmov.f32 %1, 0f00000000;\n\t"
+        "@q ld.shared.v2.f32 {%0, %1}, [%2];\n\t}"
+        : "=f"(v.x), "=f"(v.y)
         : "r"(smem_addr(p)), "r"(static_cast<int>(pred))
         : "memory");
     return v;
@@ -228,26 +241,33 @@ __host__ __device__ inline int slab_node_rows(int G, int H, int s) {
 constexpr int kSlabShift = 24;
 constexpr int kOffMask = (1 << kSlabShift) - 1;
 
-// preamble (grid.hpp:87-101) from grid constants held in shared memory: cell
-// index (bit-exact, thresholds) and the four weights in fp64, reference order
-// (a*c*inv == (a*c)*inv), rounded to fp32. Returns the packed node offset.
+// preamble (grid.hpp:87-101) in normalized cell coordinates, from grid
+// constants held in shared memory: the cell index (bit-exact, thresholds) and
+// ag = {alpha, gamma} = {a / h1, c / h2} (gaps and inverse widths in fp64,
+// rounded to fp32). The reference weights are the bilinear products
+// w00 = a c inv = alpha gamma, w10 = (1 - alpha) gamma, w01 = alpha (1 - gamma),
+// w11 = (1 - alpha)(1 - gamma), since inv_areas = 1 / (h1 h2) (grid.hpp:58-64)
+// and a + b = h1, c + d = h2 (weights_ag). Two floats per record instead of
+// four: one 1-wavefront LDS.64 per row in the gather loop. Returns the packed
+// slab / node offset.
 template <typename XT>
-__device__ __forceinline__ int locate_record(XT x1, XT x2, const XT* thr, const double* pts, const double* inv,
-                                             int G, int L, int OT, int H, float4& w) {
+__device__ __forceinline__ int locate_ag(XT x1, XT x2, const XT* thr, const double* pts, const double* invh, int G,
+                                         int L, int OT, int H, float2& ag) {
     const int i1 = cell_index_fast<XT>(x1, thr, G, L);
     const int i2 = cell_index_fast<XT>(x2, thr, G, L);
-    const double d1 = static_cast<double>(x1), d2 = static_cast<double>(x2);
-    const double a = __dsub_rn(pts[i1 + 1], d1);
-    const double b = __dsub_rn(d1, pts[i1]);
-    const double c = __dsub_rn(pts[i2 + 1], d2);
-    const double d = __dsub_rn(d2, pts[i2]);
-    const double iv = inv[i1 * G + i2];
-    w.x = __double2float_rn(__dmul_rn(__dmul_rn(a, c), iv));
-    w.y = __double2float_rn(__dmul_rn(__dmul_rn(b, c), iv));
-    w.z = __double2float_rn(__dmul_rn(__dmul_rn(a, d), iv));
-    w.w = __double2float_rn(__dmul_rn(__dmul_rn(b, d), iv));
+    ag.x = __double2float_rn(__dmul_rn(__dsub_rn(pts[i1 + 1], static_cast<double>(x1)), invh[i1]));
+    ag.y = __double2float_rn(__dmul_rn(__dsub_rn(pts[i2 + 1], static_cast<double>(x2)), invh[i2]));
     const int s = i1 / H;
     return (s << kSlabShift) | (((i1 - s * H) * (G + 1) + i2) * OT);
+}
+
+// The four bilinear weights {w00, w10, w01, w11} of a record (see locate_ag).
+// For in-cell inputs they are the reference weights to ~1 fp32 ulp; on the
+// unbounded edge cells (alpha or gamma outside [0, 1]) they extrapolate
+// exactly like the reference's (grid.hpp:79-81) and still sum to 1.
+__device__ __forceinline__ float4 weights_ag(float2 ag) {
+    const float b = 1.f - ag.x, d = 1.f - ag.y;
+    return make_float4(ag.x * ag.y, b * ag.y, ag.x * d, b * d);
 }
 
 // Kernel variants of the layer forward.
@@ -305,10 +325,10 @@ __host__ __device__ inline int staged_nrec(int nbuf, int S) { return (nbuf - 1 +
 
 // Shared-memory carve-up (host and device agree on it).
 //   sheets : NBUF x slab buffers of (H+1)(G+1) x OT fp32 (bulk-copy destinations)
-//   records: NREC x {R float4 weights, OBLK packed offsets}; NREC = staged_nrec
+//   records: NREC x {R float2 {alpha, gamma}, OBLK packed offsets}; NREC = staged_nrec
 //            when staged (they arrive with a pair's first slab), else 1
 //            (warp-private, written by the in-kernel locate)
-//   grid constants (not staged): thresholds, points[G+1], inv_areas[G*G] (fp64)
+//   grid constants (not staged): thresholds, points[G+1], inv_h[G] (fp64)
 //   NBUF "landed" mbarriers + NBUF finished-warp counters
 struct FusedSmem {
     uint32_t sheet_bytes, recw_bytes, reco_bytes, off_recw, off_reco, off_thr, off_pts, off_inv, off_bar,
@@ -323,7 +343,7 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
     FusedSmem s;
     s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
     s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * OT * 4u;
-    s.recw_bytes = sh.R * 16u;
+    s.recw_bytes = sh.R * 8u;  // float2 {alpha, gamma} per row
     s.reco_bytes = sh.OBLK * 4u;
     uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
     o = (o + 127u) & ~127u;
@@ -341,7 +361,7 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
         o += (kMaxThr + 1) * 8u;
         o = (o + 15u) & ~15u;
         s.off_inv = o;
-        o += static_cast<uint32_t>(G) * G * 8u;
+        o += static_cast<uint32_t>(G) * 8u;  // inv_h
         o = (o + 15u) & ~15u;
     }
     s.off_bar = o;
@@ -355,24 +375,24 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
 // K1 (staged path): cell records for every (pair, row) in the order K2 consumes
 // them. A CTA stages a 64-row x 16-pair X tile through shared memory (row-
 // contiguous loads), locates each (row, pair) and writes
-//   W[p][row]                        = {w00, w10, w01, w11}      (coalesced)
+//   W[p][row]                        = {alpha, gamma}            (coalesced)
 //   O[p][tile][offset_slot(row % R)] = packed slab / node offset
 // Rows in [rows, rows_pad) get zero records (their outputs are discarded).
 template <typename XT>
 __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
-                                                      int H, float4* __restrict__ W, int* __restrict__ O,
+                                                      int H, float2* __restrict__ W, int* __restrict__ O,
                                                       const InputMap im) {
     __shared__ XT xs[64][33];
     __shared__ int64_t rbase[64];
     __shared__ int coff[32];
     __shared__ XT thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
-    extern __shared__ double inv[];  // G*G
+    __shared__ double invh[kMaxThr];
     const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
     for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
-    for (int k = tid; k < G * G; k += 256) inv[k] = gc.inv_areas[k];
+    for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
     const int p0 = blockIdx.y * 16;
     const int64_t tiles = rows_pad >> sh.lgR;
     // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
@@ -404,11 +424,11 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
             if (p >= pairs) continue;
             const int64_t g = r0 + r;
             if (g >= rows_pad) continue;  // row tiles (R) may be shorter than the 64-row X tile
-            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            float2 ag = make_float2(0.f, 0.f);
             int packed = 0;
             if (g < rows)
-                packed = locate_record<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, inv, G, gc.L, sh.OT, H, w);
-            W[static_cast<size_t>(p) * rows_pad + g] = w;
+                packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.OT, H, ag);
+            W[static_cast<size_t>(p) * rows_pad + g] = ag;
             const int64_t tile = g >> sh.lgR;
             const int qc = static_cast<int>(g & (sh.R - 1));
             O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
@@ -431,8 +451,9 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 //   * fused mode: every warp locates the cells of its own rows for the next pair
 //     into a warp-private record slice (x pair prefetched a pair ahead).
 //   * gather: lane group `sub` handles one row, lane c4 a float4 of outputs; per
-//     row one LDS.128 of weights and 4 LDS.128 of coefficients (nodes n, n+1,
-//     n+G+1, n+G+2), 16 FMAs; a lane group's RT node offsets are contiguous
+//     row one LDS.64 of {alpha, gamma} (one wavefront for the warp's rows; an
+//     LDS.128 of four weights would cost two) and 4 LDS.128 of coefficients
+//     (nodes n, n+1, n+G+1, n+G+2), 16 FMAs; a lane group's RT node offsets are contiguous
 //     (int4 loads, kept in registers across the pair's slabs). With slabs
 //     (SLAB = true) a row is gathered only during its cell's slab.
 //
@@ -444,7 +465,7 @@ template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
-                     const __grid_constant__ GridConst gc, const float4* __restrict__ recW,
+                     const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im) {
     using Sh = FusedShape<OT, RT, NW>;
     constexpr int R = Sh::R;
@@ -456,7 +477,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int H = (G + S - 1) / S;
     const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW);
     float* sheets = reinterpret_cast<float*>(smem);
-    float4* rec_w = reinterpret_cast<float4*>(smem + L.off_recw);
+    float2* rec_w = reinterpret_cast<float2*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
     XT* thr = reinterpret_cast<XT*>(smem + L.off_thr);
     double* pts = reinterpret_cast<double*>(smem + L.off_pts);
@@ -479,7 +500,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if constexpr (MODE != kModeStaged) {
         for (int k = tid; k < kMaxThr; k += NT) thr[k] = thr_of<XT>(gc)[k];
         for (int k = tid; k <= G; k += NT) pts[k] = gc.points[k];
-        for (int k = tid; k < G * G; k += NT) inv[k] = gc.inv_areas[k];
+        for (int k = tid; k < G; k += NT) inv[k] = gc.inv_h[k];
     }
     uint64_t policy = 0, policy_rec = 0;
     if constexpr (kSmemSheet) {
@@ -562,11 +583,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
         for (int k = 0; k < Sh::LOC; ++k) {
             const int q = k * 32 + lane;
             if (q < Sh::ROWS_W) {
-                float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+                float2 ag = make_float2(0.f, 0.f);
                 int packed = 0;
-                if (xrow[k]) packed = locate_record<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, OT, H, w);
+                if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, OT, H, ag);
                 const int qc = warp * Sh::ROWS_W + q;
-                rec_w[qc] = w;
+                rec_w[qc] = ag;
                 rec_o[offset_slot(shp, qc)] = packed;
             }
         }
@@ -584,7 +605,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         __syncwarp();
     }
     int offs[RT];
-    const float4* rw = rec_w;
+    const float2* rw = rec_w;
     int p = 0, s = 0;
     for (int u = 0; u < units; ++u) {
         const float* sh;
@@ -597,7 +618,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets to registers (kept across slabs)
             const int rs = MODE == kModeStaged ? p % L.nrec : 0;
-            rw = rec_w + rs * (L.recw_bytes / 16) + warp * Sh::ROWS_W + sub;
+            rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
             const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
 #pragma unroll
             for (int k = 0; k < RT / 4; ++k) {
@@ -616,13 +637,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 const bool v = (offs[j] >> kSlabShift) == s;
                 const float* b0 = sh + (offs[j] & kOffMask);
                 const float* b1 = b0 + rstride;
-                w = lds128_if(rw + j * Sh::RPW, v);
+                w = weights_ag(lds64_if(rw + j * Sh::RPW, v));
                 p00 = lds128_if(b0, v);
                 p01 = lds128_if(b0 + OT, v);
                 p10 = lds128_if(b1, v);
                 p11 = lds128_if(b1 + OT, v);
             } else {
-                w = rw[j * Sh::RPW];
+                w = weights_ag(rw[j * Sh::RPW]);
                 const float* b0 = sh + offs[j];
                 const float* b1 = b0 + rstride;
                 if constexpr (kSmemSheet) {
@@ -702,7 +723,7 @@ constexpr int kNarrowThreads = 1024;
 __host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) {
     const uint32_t tab = static_cast<uint32_t>((G + 1) * (G + 1)) * pairs * NO * 4u;
     uint32_t o = (tab + 15u) & ~15u;
-    o += kMaxThr * 8u + (kMaxThr + 1) * 8u + static_cast<uint32_t>(G) * G * 8u + 16u;
+    o += kMaxThr * 8u + (kMaxThr + 1) * 8u + static_cast<uint32_t>(G) * 8u + 16u;
     return (o + 127u) & ~127u;
 }
 
@@ -721,12 +742,12 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
     double* pts = reinterpret_cast<double*>(smem + o);
     o += (kMaxThr + 1) * 8u;
     double* inv = reinterpret_cast<double*>(smem + o);
-    o += static_cast<uint32_t>(G) * G * 8u;
+    o += static_cast<uint32_t>(G) * 8u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((o + 7u) & ~7u));
     const int tid = threadIdx.x;
     for (int k = tid; k < kMaxThr; k += kNarrowThreads) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += kNarrowThreads) pts[k] = gc.points[k];
-    for (int k = tid; k < G * G; k += kNarrowThreads) inv[k] = gc.inv_areas[k];
+    for (int k = tid; k < G; k += kNarrowThreads) inv[k] = gc.inv_h[k];
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
@@ -748,8 +769,9 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
         for (int q = 0; q < NO; ++q) acc[q] = 0.f;
         const XT* xr = X + in_rowbase(im, r, n_in);
         auto one_pair = [&](int p, XT x1, XT x2) {
-            float4 w;
-            const int off = locate_record<XT>(x1, x2, thr, pts, inv, G, gc.L, NO, G, w);
+            float2 ag;
+            const int off = locate_ag<XT>(x1, x2, thr, pts, inv, G, gc.L, NO, G, ag);
+            const float4 w = weights_ag(ag);
             const float* b = tab + static_cast<size_t>(p) * nodes * NO + off;
 #pragma unroll
             for (int q = 0; q < NO; ++q)

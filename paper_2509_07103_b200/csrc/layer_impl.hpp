@@ -35,7 +35,7 @@ struct Plan {
 // (definitions in launch_gather.cuh, instantiated in gather_ot{16,32,64}.cu).
 template <int OT, typename XT>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
-                          const float4* recW, const int* recO, const InputMap& im, cudaStream_t st);
+                          const float2* recW, const int* recO, const InputMap& im, cudaStream_t st);
 
 // Entry points shared with the other host translation units (model.cu):
 // defined in lmkan_b200.cu next to the layer C-ABI.

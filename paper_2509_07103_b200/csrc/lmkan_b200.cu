@@ -222,11 +222,11 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
         if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: narrow kernel launch");
         return LMKAN_B200_OK;
     }
-    float4* recW = nullptr;
+    float2* recW = nullptr;
     int* recO = nullptr;
     if (pl.mode == kModeStaged) {
         // K1: cell records, stream-ordered scratch (pool memory is retained, see alloc_layer)
-        const size_t wbytes = static_cast<size_t>(L->pairs) * pl.rows_pad * sizeof(float4);
+        const size_t wbytes = static_cast<size_t>(L->pairs) * pl.rows_pad * sizeof(float2);
         const size_t obytes = static_cast<size_t>(L->pairs) * pl.row_tiles * pl.sh.OBLK * sizeof(int);
         CK(cudaMallocAsync(reinterpret_cast<void**>(&recW), wbytes, st));
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&recO), obytes, st);
@@ -238,7 +238,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
         const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
-        records_kernel<XT><<<g1, 256, sizeof(double) * L->G * L->G, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
+        records_kernel<XT><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
                                                                             pl.sh, H, recW, recO, im);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
@@ -277,7 +277,7 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory (G too large)");
     int64_t chunk = rows;
     if (pl.mode == kModeStaged) {
-        const size_t per_row = static_cast<size_t>(L->pairs) * (sizeof(float4) + sizeof(int) * 2);
+        const size_t per_row = static_cast<size_t>(L->pairs) * (sizeof(float2) + sizeof(int) * 2);
         const int64_t max_rows = static_cast<int64_t>(record_scratch_cap() / per_row) / pl.sh.R * pl.sh.R;
         if (rows > max_rows) chunk = std::max<int64_t>(max_rows, pl.sh.R);
     }
@@ -366,6 +366,7 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
         gc.t64[k] = k < G - 1 ? t64[k] : dnan;
     }
     for (int k = 0; k <= kMaxThr; ++k) gc.points[k] = k <= G ? pts[k] : 0.0;
+    for (int k = 0; k < kMaxThr; ++k) gc.inv_h[k] = k < G ? 1.0 / (pts[k + 1] - pts[k]) : 0.0;
     L->table_bytes = static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->OT * sizeof(float);
     cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
     if (e == cudaSuccess)

@@ -40,22 +40,22 @@ __global__ void __launch_bounds__(512, 1) lds_bench(int iters, uint32_t seed, fl
     uint32_t sv = lane, accu = 0;
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+        row = (row + 37u) & 127u;
+        const uint32_t a = lb + (row << 9);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            row = (row + 37u) & 255u;
-            const uint32_t a = lb + (row << 9);
             uint32_t x = 0, y = 0, z = 0, w = 0;
             if (P <= 4 || P == 9) {
-                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a) : "memory");
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a + k * 8192) : "memory");
             } else if (P == 5 || P == 13) {
-                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x) : "r"(a) : "memory");
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x) : "r"(a + k * 8192) : "memory");
             } else if (P == 6) {
-                asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(y) : "r"(sv), "r"(row & 31));
+                asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(y) : "r"(sv), "r"((row + k) & 31));
             } else if (P == 7) {
-                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a) : "memory");
-                asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(y) : "r"(sv), "r"(row & 31));
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a + k * 8192) : "memory");
+                asm volatile("shfl.sync.idx.b32 %0, %1, %2, 31, -1;" : "=r"(y) : "r"(sv), "r"((row + k) & 31));
             } else if (P == 8 || P == 10 || P == 11) {
-                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a) : "memory");
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a + k * 8192) : "memory");
             }
             accu ^= x ^ y ^ z ^ w;
         }
