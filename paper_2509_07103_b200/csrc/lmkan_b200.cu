@@ -98,22 +98,23 @@ int env_int(const char* name, int dflt) {
 }
 
 // Output tile width for a layer: the widest of {64, 32, 16} (not padding a
-// small layer by 2x or more) whose sheet can be double-buffered in shared
-// memory with at most kMaxSlabs i1-slabs; else the narrowest single-buffered.
+// small layer by 2x or more) whose whole sheet can be double-buffered in shared
+// memory; only if none can, the fewest i1-slabs (up to 3) that double-buffer,
+// else the narrowest single-buffered. Unslabbed wins over wider: a slabbed
+// sheet makes every row issue (predicated-off) loads in every slab (measured at
+// G = 28: OT 32 unslabbed 7.0 ms, OT 16 8.6 ms, OT 32 two slabs 11.2 ms).
 int choose_out_tile(int n_out, int G, int smem_cap) {
     const int v = env_int("LMKAN_B200_OT", 0);
     if (v == 16 || v == 32 || v == 64) return v;
-    // Large grids: the (G+1)^2-node sheet streamed per pair dominates, so the
-    // tallest row tile (OT = 16 -> 2048 rows per CTA) wins (measured at G = 28).
-    if (G >= 24) return 16;
     for (int want_buf : {2, 1}) {
-        for (int OT : {64, 32, 16}) {
-            if (OT > 16 && OT / 2 >= n_out) continue;
-            for (int S = 1; S <= (want_buf == 2 ? 3 : 1); ++S)
+        for (int S = 1; S <= (want_buf == 2 ? 3 : 1); ++S) {
+            for (int OT : {64, 32, 16}) {
+                if (OT > 16 && OT / 2 >= n_out) continue;
                 for (int RT : kRTChoices) {
                     const FusedSmem s = fused_smem_layout(G, OT, RT, want_buf, kModeStaged, S);
                     if (static_cast<int>(s.total) <= smem_cap) return OT;
                 }
+            }
         }
     }
     return 16;
