@@ -257,7 +257,7 @@ __device__ __forceinline__ int locate_ag(XT x1, XT x2, const XT* thr, const doub
     const int i2 = cell_index_fast<XT>(x2, thr, G, L);
     ag.x = __double2float_rn(__dmul_rn(__dsub_rn(pts[i1 + 1], static_cast<double>(x1)), invh[i1]));
     ag.y = __double2float_rn(__dmul_rn(__dsub_rn(pts[i2 + 1], static_cast<double>(x2)), invh[i2]));
-    const int s = i1 / H;
+    const int s = (i1 >= H) + (i1 >= 2 * H) + (i1 >= 3 * H);  // slab (S <= 4), no integer division
     return (s << kSlabShift) | (((i1 - s * H) * (G + 1) + i2) * OT);
 }
 
@@ -394,9 +394,10 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
     for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
     const int p0 = blockIdx.y * 16;
+    const int r = tid & 63, pq = tid >> 6;
     const int64_t tiles = rows_pad >> sh.lgR;
     // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
-    // (thresholds, points, G*G inverse areas) is amortized over many tiles
+    // (thresholds, points, inverse widths) is amortized over many tiles
     for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64; r0 < rows_pad; r0 += static_cast<int64_t>(gridDim.x) * 64) {
         __syncthreads();  // previous tile's xs / rbase fully consumed
         if (tid < 64) rbase[tid] = in_rowbase(im, r0 + tid, n_in);
@@ -406,9 +407,9 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             const int i = tid + 256 * t;
-            const int r = i >> 5, c = i & 31;
+            const int rr = i >> 5, c = i & 31;
             const int col = 2 * p0 + c;
-            v[t] = (r0 + r < rows && col < n_in) ? __ldg(X + rbase[r] + coff[c]) : XT(0);
+            v[t] = (r0 + rr < rows && col < n_in) ? __ldg(X + rbase[rr] + coff[c]) : XT(0);
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -416,22 +417,30 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
             xs[i >> 5][i & 31] = v[t];
         }
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int idx = tid + 256 * k;
-            const int r = idx & 63, pl = idx >> 6;
-            const int p = p0 + pl;
-            if (p >= pairs) continue;
-            const int64_t g = r0 + r;
-            if (g >= rows_pad) continue;  // row tiles (R) may be shorter than the 64-row X tile
-            float2 ag = make_float2(0.f, 0.f);
-            int packed = 0;
-            if (g < rows)
-                packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.OT, H, ag);
-            W[static_cast<size_t>(p) * rows_pad + g] = ag;
+        // thread = (row r of the tile, pairs pq, pq+4, pq+8, pq+12 of the block):
+        // the row's tile / offset slot are computed once, record addresses step
+        // by whole pairs
+        const int64_t g = r0 + r;
+        if (g < rows_pad) {  // row tiles (R) may be shorter than the 64-row X tile
             const int64_t tile = g >> sh.lgR;
-            const int qc = static_cast<int>(g & (sh.R - 1));
-            O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + offset_slot(sh, qc)] = packed;
+            const int slot = offset_slot(sh, static_cast<int>(g & (sh.R - 1)));
+            float2* wp = W + static_cast<size_t>(p0 + pq) * rows_pad + g;
+            int* op = O + (static_cast<size_t>(p0 + pq) * tiles + tile) * sh.OBLK + slot;
+            const size_t wstep = static_cast<size_t>(4) * rows_pad, ostep = static_cast<size_t>(4) * tiles * sh.OBLK;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int pl = pq + 4 * k;
+                if (p0 + pl < pairs) {
+                    float2 ag = make_float2(0.f, 0.f);
+                    int packed = 0;
+                    if (g < rows)
+                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.OT, H, ag);
+                    *wp = ag;
+                    *op = packed;
+                }
+                wp += wstep;
+                op += ostep;
+            }
         }
     }
 }
