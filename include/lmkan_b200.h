@@ -163,6 +163,22 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, in
 int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
                     int* nbuf, int* rows_per_cta, int* launches, int* mode, int* slabs, int* warps_per_cta);
 
+/* ---- training path ----
+ *
+ * lmkan_backward (layer.hpp:141-202) in fp64: dP_dev (the fp64 table layout
+ * [i1][i2][pair][out], (G+1)^2 * (n_in/2) * n_out doubles) is ADDED into, as
+ * the reference does; dX_dev [rows][n_in] may be NULL. P_dev is the fp64
+ * master table in reference layout (the layer handle supplies grid and gamma;
+ * its fp32 table is forward-only). Rows are accumulated in order and each dX
+ * entry sums outputs in order with the reference's expression grouping, so dP
+ * and dX are bit-identical to the reference's lmkan_backward with workers = 1
+ * (and deterministic). EINVAL for output-sliced layers. */
+int lmkan_b200_backward_f64(const lmkan_b200_layer* layer, const double* P_dev, const double* X_dev,
+                            const double* dY_dev, double* dP_dev, double* dX_dev, int64_t rows, void* stream);
+/* Same with host arrays (synchronous); `workers` accepted and ignored. */
+int lmkan_b200_backward_host_f64(const lmkan_b200_layer* layer, const double* P, const double* X,
+                                 const double* dY, double* dP, double* dX, int64_t rows, size_t workers);
+
 /* ---- models: the LMK1 container and the pure-lookup inference chain ----
  *
  * load_model (serialize.hpp:185-301) reads "LMK1" | u32 LE header length |

@@ -150,6 +150,55 @@ void lmko_forward(int n_in, int n_out, int G, const double* points, const double
     free(tid);
 }
 
+/* layer.hpp:141-202, one worker (the row loop of worker 0 accumulates straight
+ * into dP, layer.hpp:162-163; the per-q loop order and expression grouping of
+ * layer.hpp:182-191 are kept, so with -ffp-contract=off this is bit-identical
+ * to the reference at workers = 1). */
+void lmko_backward(int n_in, int n_out, int G, const double* points, const double* inv_areas,
+                   const double* P, double gamma, const double* X, const double* dY, int64_t rows,
+                   double* dP, double* dX) {
+    const int pairs = n_in / 2;
+    const int G1 = G + 1;
+    const size_t per_node = (size_t)pairs * n_out;
+    for (int64_t r = 0; r < rows; ++r) {
+        const double* x = X + r * n_in;
+        const double* g = dY + r * n_out;
+        for (int p = 0; p < pairs; ++p) {
+            int i1, i2;
+            double w[4];
+            lmko_preamble(G, points, inv_areas, x[2 * p], x[2 * p + 1], &i1, &i2, w);
+            const size_t base = ((size_t)i1 * G1 + i2) * per_node + (size_t)p * n_out;
+            double* d00 = dP + base;
+            double* d10 = dP + base + (size_t)G1 * per_node;
+            double* d01 = dP + base + per_node;
+            double* d11 = d10 + per_node;
+            const double* p00 = P + base;
+            const double* p10 = p00 + (size_t)G1 * per_node;
+            const double* p01 = p00 + per_node;
+            const double* p11 = p10 + per_node;
+            const double inv = inv_areas[i1 * G + i2];
+            const double r2 = points[i2 + 1] - x[2 * p + 1];
+            const double l2 = x[2 * p + 1] - points[i2];
+            const double r1 = points[i1 + 1] - x[2 * p];
+            const double l1 = x[2 * p] - points[i1];
+            double acc1 = 0.0, acc2 = 0.0;
+            for (int q = 0; q < n_out; ++q) {
+                const double gq = gamma * g[q];
+                d00[q] += w[0] * gq;
+                d10[q] += w[1] * gq;
+                d01[q] += w[2] * gq;
+                d11[q] += w[3] * gq;
+                acc1 += gq * ((p10[q] - p00[q]) * r2 + (p11[q] - p01[q]) * l2);
+                acc2 += gq * ((p01[q] - p00[q]) * r1 + (p11[q] - p10[q]) * l1);
+            }
+            if (dX) {
+                dX[r * n_in + 2 * p] = acc1 * inv;
+                dX[r * n_in + 2 * p + 1] = acc2 * inv;
+            }
+        }
+    }
+}
+
 /* ---- threshold derivation (not in the reference; derived FROM it) ---- */
 
 /* Monotone maps between finite floating values and unsigned keys. */

@@ -40,6 +40,14 @@ void lmko_forward(int n_in, int n_out, int G, const double* points, const double
                   const double* P, double gamma, const double* X, int64_t rows, double* Y,
                   int threads);
 
+/* layer.hpp:141-202 (lmkan_backward) with one worker: dP (same layout as P)
+ * accumulates gamma * w * dY at the four nodes of every (row, pair), rows in
+ * order; dX [rows][n_in] (may be NULL) from the analytic cell derivatives.
+ * dP must hold its initial value (the reference adds into it). */
+void lmko_backward(int n_in, int n_out, int G, const double* points, const double* inv_areas,
+                   const double* P, double gamma, const double* X, const double* dY, int64_t rows,
+                   double* dP, double* dX);
+
 /* Threshold table derived from lmko_interval_index by bisection over the total
  * order of finite doubles / floats: t[k-1] = min{x : interval_index(x) >= k},
  * k = 1..G-1. Assumes interval_index is monotone in x, which

@@ -47,6 +47,7 @@ class Port:
         L.lmko_preamble.argtypes = [C.c_int, _P, _P, C.c_double, C.c_double, _P, _P, _P]
         L.lmko_locate.argtypes = [C.c_int, _P, _P, C.c_int, _P, C.c_int64, _P, _P, _P]
         L.lmko_forward.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_double, _P, C.c_int64, _P, C.c_int]
+        L.lmko_backward.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_double, _P, _P, C.c_int64, _P, _P]
         L.lmko_thresholds_f64.argtypes = [C.c_int, _P]
         L.lmko_thresholds_f32.argtypes = [C.c_int, _P]
         L.lmko_verify_thresholds_f32.restype = C.c_int64
@@ -86,6 +87,21 @@ class Port:
         self.L.lmko_forward(n_in, n_out, G, _p(pts), _p(inv), _p(P), float(gamma), _p(X), rows, _p(Y), threads)
         return Y
 
+    def backward(self, G: int, P: np.ndarray, X: np.ndarray, dY: np.ndarray, gamma: float = 1.0,
+                 dP0: np.ndarray = None, workers: int = 1):
+        """lmkan_backward (layer.hpp:141-202), one worker: (dP0 + dP, dX)."""
+        X = np.ascontiguousarray(X, np.float64)
+        dY = np.ascontiguousarray(dY, np.float64)
+        P = np.ascontiguousarray(P, np.float64)
+        rows, n_in = X.shape
+        n_out = dY.shape[1]
+        pts, inv = self.build_grid(G)
+        dP = np.zeros(P.shape) if dP0 is None else np.array(dP0, np.float64, copy=True)
+        dX = np.zeros((rows, n_in))
+        self.L.lmko_backward(n_in, n_out, G, _p(pts), _p(inv), _p(P), float(gamma), _p(X), _p(dY), rows, _p(dP),
+                             _p(dX))
+        return dP, dX
+
     def thresholds_f64(self, G: int) -> np.ndarray:
         t = np.zeros(G - 1)
         self.L.lmko_thresholds_f64(G, _p(t))
@@ -124,6 +140,7 @@ class Ref:
         L.lmkref_matrix_destroy.argtypes = [_P]
         L.lmkref_matrix_read.argtypes = [_P, _P]
         L.lmkref_forward.argtypes = [_P, _P, _P, C.c_uint64]
+        L.lmkref_backward.argtypes = [_P, _P, _P, _P, _P, C.c_uint64]
         L.lmkref_worker_count.restype = C.c_uint64
         self.L = L
 
@@ -166,6 +183,33 @@ class Ref:
             return lay.forward(X, workers)
         finally:
             lay.close()
+
+
+def _ref_backward(self, G, P, X, dY, gamma=1.0, dP0=None, workers=1):
+    """The reference's lmkan_backward (layer.hpp:141-202): (dP0 + dP, dX)."""
+    X = np.ascontiguousarray(X, np.float64)
+    dY = np.ascontiguousarray(dY, np.float64)
+    P = np.ascontiguousarray(P, np.float64)
+    rows, n_in = X.shape
+    n_out = dY.shape[1]
+    lay = RefLayer(self, n_in, n_out, G, P, gamma)
+    dP = np.zeros(P.shape) if dP0 is None else np.array(dP0, np.float64, copy=True)
+    xm = self.L.lmkref_matrix_create(rows, n_in, _p(X))
+    gm = self.L.lmkref_matrix_create(rows, n_out, _p(dY))
+    dxm = self.L.lmkref_matrix_create(rows, n_in, None)
+    try:
+        if self.L.lmkref_backward(lay.h, xm, gm, _p(dP), dxm, workers) != 0:
+            raise ValueError(self.L.lmkref_last_error().decode())
+        dX = np.zeros((rows, n_in))
+        self.L.lmkref_matrix_read(dxm, _p(dX))
+        return dP, dX
+    finally:
+        for m in (xm, gm, dxm):
+            self.L.lmkref_matrix_destroy(m)
+        lay.close()
+
+
+Ref.backward = _ref_backward
 
 
 class RefLayer:

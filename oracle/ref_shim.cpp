@@ -6,6 +6,7 @@
 // build_grid (grid.hpp:44-68) and init_layer (layer.hpp:69-86).
 #include <cstdint>
 #include <cstring>
+#include <vector>
 #include <exception>
 #include <string>
 
@@ -126,6 +127,22 @@ int lmkref_forward(const void* layer, const void* X, void* Y, uint64_t workers) 
         lmkan::lmkan_forward(*static_cast<const lmkan::LmKanLayer*>(layer),
                              *static_cast<const lmkan::Matrix*>(X), *static_cast<lmkan::Matrix*>(Y),
                              workers);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// lmkan_backward (layer.hpp:141-202): dP (layer.P.size() doubles) is added
+// into, dX [rows][n_in] or NULL.
+int lmkref_backward(const void* layer, const void* X, const void* dY, double* dP, void* dX, uint64_t workers) {
+    try {
+        const auto& L = *static_cast<const lmkan::LmKanLayer*>(layer);
+        std::vector<double> acc(dP, dP + L.P.size());
+        lmkan::lmkan_backward(L, *static_cast<const lmkan::Matrix*>(X), *static_cast<const lmkan::Matrix*>(dY), acc,
+                              static_cast<lmkan::Matrix*>(dX), workers);
+        std::memcpy(dP, acc.data(), sizeof(double) * acc.size());
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

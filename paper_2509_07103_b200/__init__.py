@@ -221,6 +221,39 @@ class Layer:
         check(fn(self._h, _ptr(X), _ptr(i1), _ptr(i2), _ptr(w), int(rows), _stream_ptr(stream)))
         return i1, i2, w
 
+    # -- training path ------------------------------------------------------
+    def backward(self, P, X, dY, dP=None, want_dx: bool = True, stream=None):
+        """lmkan_backward (layer.hpp:141-202) in fp64. CUDA tensors: P (the fp64
+        master table, reference layout), X [rows, n_in], dY [rows, n_out];
+        dP is added into (zeros when None). Returns (dP, dX or None).
+        numpy arrays in -> the synchronous host path, numpy out."""
+        if isinstance(X, np.ndarray):
+            P = np.ascontiguousarray(P, np.float64)
+            X = np.ascontiguousarray(X, np.float64)
+            dY = np.ascontiguousarray(dY, np.float64)
+            dP = np.zeros(P.shape) if dP is None else np.ascontiguousarray(dP, np.float64)
+            dX = np.zeros(X.shape) if want_dx else None
+            check(lib.lmkan_b200_backward_host_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX),
+                                                   int(X.shape[0]), 0))
+            return dP, dX
+        import torch
+        for t in (P, X, dY):
+            assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+        if X.shape[1] != self.n_in:
+            raise ValueError(f"lmkan_backward: expected width {self.n_in}, got {X.shape[1]}")
+        if dY.shape[1] != self.n_out:
+            raise ValueError(f"lmkan_backward: expected width {self.n_out}, got {dY.shape[1]}")
+        if dY.shape[0] != X.shape[0]:
+            raise ValueError("lmkan_backward: X and dY row counts differ")
+        if dP is None:
+            dP = torch.zeros_like(P)
+        elif dP.numel() != P.numel():
+            raise ValueError("lmkan_backward: dP size mismatch")
+        dX = torch.empty_like(X) if want_dx else None
+        check(lib.lmkan_b200_backward_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX), int(X.shape[0]),
+                                          _stream_ptr(stream)))
+        return dP, dX
+
     # -- introspection ------------------------------------------------------
     def set_gamma(self, gamma: float) -> None:
         check(lib.lmkan_b200_layer_set_gamma(self._h, float(gamma)))

@@ -208,3 +208,24 @@ def test_thresholds_exhaustive_G16(port):
     """All 2^32 fp32 bit patterns (about 15 s on 8 cores)."""
     t = port.thresholds_f32(16)
     assert port.verify_thresholds_f32(16, t, 0, 0xFFFFFFFF, threads=os.cpu_count() or 8) == 0
+
+
+def test_backward_port_bitwise_vs_reference():
+    """The C restatement of lmkan_backward (lmko_backward) is bit-identical to
+    the reference's (layer.hpp:141-202) at workers = 1, dP += semantics included."""
+    import pyoracle
+    try:
+        ref = pyoracle.Ref()
+    except (FileNotFoundError, OSError):
+        pytest.skip("oracle/_ref not built")
+    port = pyoracle.Port()
+    for (n_in, n_out, G, rows) in [(2, 1, 4, 16), (6, 5, 3, 40), (8, 6, 12, 33), (12, 16, 28, 64)]:
+        rng = np.random.default_rng(G + n_in)
+        P = rng.standard_normal((G + 1, G + 1, n_in // 2, n_out))
+        X = rng.standard_normal((rows, n_in)) * 1.5
+        X[::5, 0] = 80.0
+        dY = rng.standard_normal((rows, n_out))
+        dP0 = rng.standard_normal(P.shape)
+        a = ref.backward(G, P, X, dY, 0.7, dP0=dP0, workers=1)
+        b = port.backward(G, P, X, dY, 0.7, dP0=dP0)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
