@@ -169,13 +169,19 @@ int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, 
  * [i1][i2][pair][out], (G+1)^2 * (n_in/2) * n_out doubles) is ADDED into, as
  * the reference does; dX_dev [rows][n_in] may be NULL. P_dev is the fp64
  * master table in reference layout (the layer handle supplies grid and gamma;
- * its fp32 table is forward-only). Rows are accumulated in order and each dX
- * entry sums outputs in order with the reference's expression grouping, so dP
- * and dX are bit-identical to the reference's lmkan_backward with workers = 1
- * (and deterministic). EINVAL for output-sliced layers. */
+ * its fp32 table is forward-only). `workers` has the reference's meaning: rows
+ * are split into that many contiguous chunks (threading.hpp:33-39), each
+ * chunk's dP contributions summed in row order, chunk partials merged in
+ * worker order, dX summed over outputs in order with the reference's
+ * expression grouping — so dP and dX are BIT-IDENTICAL to the reference's
+ * lmkan_backward with the same `workers`. workers = 0 picks a count that fills
+ * the GPU (lmkan_b200_backward_workers). EINVAL for output-sliced layers. */
 int lmkan_b200_backward_f64(const lmkan_b200_layer* layer, const double* P_dev, const double* X_dev,
-                            const double* dY_dev, double* dP_dev, double* dX_dev, int64_t rows, void* stream);
-/* Same with host arrays (synchronous); `workers` accepted and ignored. */
+                            const double* dY_dev, double* dP_dev, double* dX_dev, int64_t rows,
+                            uint64_t workers, void* stream);
+/* The worker count workers = 0 selects for `rows` rows. */
+int64_t lmkan_b200_backward_workers(const lmkan_b200_layer* layer, int64_t rows);
+/* Same with host arrays (synchronous). */
 int lmkan_b200_backward_host_f64(const lmkan_b200_layer* layer, const double* P, const double* X,
                                  const double* dY, double* dP, double* dX, int64_t rows, size_t workers);
 

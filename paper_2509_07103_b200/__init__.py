@@ -222,11 +222,12 @@ class Layer:
         return i1, i2, w
 
     # -- training path ------------------------------------------------------
-    def backward(self, P, X, dY, dP=None, want_dx: bool = True, stream=None):
+    def backward(self, P, X, dY, dP=None, want_dx: bool = True, workers: int = 0, stream=None):
         """lmkan_backward (layer.hpp:141-202) in fp64. CUDA tensors: P (the fp64
         master table, reference layout), X [rows, n_in], dY [rows, n_out];
-        dP is added into (zeros when None). Returns (dP, dX or None).
-        numpy arrays in -> the synchronous host path, numpy out."""
+        dP is added into (zeros when None). Returns (dP, dX or None); bitwise
+        equal to the reference run with the same `workers` (0 = GPU-filling
+        count, see backward_workers). numpy in -> synchronous host path."""
         if isinstance(X, np.ndarray):
             P = np.ascontiguousarray(P, np.float64)
             X = np.ascontiguousarray(X, np.float64)
@@ -234,7 +235,7 @@ class Layer:
             dP = np.zeros(P.shape) if dP is None else np.ascontiguousarray(dP, np.float64)
             dX = np.zeros(X.shape) if want_dx else None
             check(lib.lmkan_b200_backward_host_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX),
-                                                   int(X.shape[0]), 0))
+                                                   int(X.shape[0]), int(workers)))
             return dP, dX
         import torch
         for t in (P, X, dY):
@@ -251,8 +252,12 @@ class Layer:
             raise ValueError("lmkan_backward: dP size mismatch")
         dX = torch.empty_like(X) if want_dx else None
         check(lib.lmkan_b200_backward_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX), int(X.shape[0]),
-                                          _stream_ptr(stream)))
+                                          int(workers), _stream_ptr(stream)))
         return dP, dX
+
+    def backward_workers(self, rows: int) -> int:
+        """Worker count (row chunks) the backward uses for workers = 0."""
+        return int(lib.lmkan_b200_backward_workers(self._h, int(rows)))
 
     # -- introspection ------------------------------------------------------
     def set_gamma(self, gamma: float) -> None:

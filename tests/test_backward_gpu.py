@@ -1,10 +1,10 @@
 """GPU: lmkan_backward (layer.hpp:141-202) on the B200 path.
 
-Bar: dP and dX BIT-IDENTICAL to the reference's own lmkan_backward with
-workers = 1 (oracle/_ref, or the C restatement when absent, itself pinned
-bitwise to the reference at workers = 1 in tests/test_oracle.py), including
-the += semantics of dP; plus the reference's own backward test cases
-(test_layer.cpp:147-226) restated.
+Bar: dP and dX BIT-IDENTICAL to the reference's own lmkan_backward run with
+the same worker count (oracle/_ref; the C restatement, pinned bitwise to the
+reference at workers = 1 in tests/test_oracle.py, covers workers = 1 when the
+reference build is absent), including the += semantics of dP; plus the
+reference's own backward test cases (test_layer.cpp:147-226) restated.
 """
 import numpy as np
 import pytest
@@ -44,16 +44,20 @@ def test_backward_bitwise_vs_reference(torch, pkg, oracle, n_in, n_out, G, rows)
     X[2::7, 0] = -1e-30      # tiny negative: cell G/2 (grid.hpp:72-75)
     gamma = 0.7
     dP0 = np.random.default_rng(1).standard_normal(P.shape)  # dP is added into
-    ref_dP, ref_dX = oracle.backward(G, P, X, dY, gamma, dP0=dP0, workers=1)
     layer = pkg.Layer.from_host(n_in, n_out, G, P, gamma)
     Pd = torch.from_numpy(P).cuda()
-    dPd = torch.from_numpy(dP0).cuda()
-    got_dP, got_dX = layer.backward(Pd, torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda(), dP=dPd)
-    assert np.array_equal(got_dP.cpu().numpy(), ref_dP)
-    assert np.array_equal(got_dX.cpu().numpy(), ref_dX)
-    # host path, same bits
-    h_dP, h_dX = layer.backward(P, X, dY, dP=dP0)
-    assert np.array_equal(h_dP, ref_dP) and np.array_equal(h_dX, ref_dX)
+    Xd, dYd = torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda()
+    import pyoracle
+    have_ref = isinstance(oracle, pyoracle.Ref)
+    for workers in ([1, 3, 0] if have_ref else [1]):
+        w = workers or layer.backward_workers(rows)
+        ref_dP, ref_dX = oracle.backward(G, P, X, dY, gamma, dP0=dP0, workers=w)
+        got_dP, got_dX = layer.backward(Pd, Xd, dYd, dP=torch.from_numpy(dP0).cuda(), workers=workers)
+        assert np.array_equal(got_dP.cpu().numpy(), ref_dP), workers
+        assert np.array_equal(got_dX.cpu().numpy(), ref_dX), workers
+        # host path, same bits
+        h_dP, h_dX = layer.backward(P, X, dY, dP=dP0, workers=workers)
+        assert np.array_equal(h_dP, ref_dP) and np.array_equal(h_dX, ref_dX)
 
 
 def test_backward_deterministic(torch, pkg):
