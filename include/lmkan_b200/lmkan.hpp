@@ -8,6 +8,9 @@
 //   LmKanLayer                      layer.hpp:24-61 (same fields and P layout)
 //   default_init_scale, init_layer  layer.hpp:63-86 (bit-identical table)
 //   lmkan_forward                   layer.hpp:108-134 (same signature)
+//   worker_count                    threading.hpp:11-19
+//   lmkan_backward                  layer.hpp:141-202 (same signature; bit-
+//                                   identical results for the same workers)
 //   FormatError                     errors.hpp:23-26
 //   load_model, model_infer         serialize.hpp:185-301, model.hpp:313-316,
 //                                   for fused pure-lookup models (DeviceModel)
@@ -25,10 +28,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../lmkan_b200.h"
@@ -240,6 +245,39 @@ inline void lmkan_forward(const LmKanLayer& layer, const Matrix& X, Matrix& Y, s
     detail::throw_status(lmkan_b200_forward_host_f64(h, X.data(), Y.data(), static_cast<std::int64_t>(X.rows()),
                                                      workers),
                          "lmkan_forward");
+}
+
+// threading.hpp:11-19: LMKAN_THREADS if set, else hardware concurrency.
+inline std::size_t worker_count() {
+    if (const char* env = std::getenv("LMKAN_THREADS")) {
+        const long n = std::strtol(env, nullptr, 10);
+        if (n >= 1) return static_cast<std::size_t>(n);
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    return hc == 0 ? 1 : hc;
+}
+
+// layer.hpp:141-202. Same checks and messages; dP is added into; dX resized
+// when its shape differs. `workers` keeps the reference's meaning (0 ->
+// worker_count()): the rows are split into that many contiguous chunks and the
+// per-chunk sums are merged in order, so the result is bit-identical to the
+// reference's lmkan_backward with the same worker count. The device runs the
+// fp64 master table P; a larger explicit `workers` spreads the dP sums over
+// more of the GPU (still matching the reference run with that count).
+inline void lmkan_backward(const LmKanLayer& layer, const Matrix& X, const Matrix& dY, std::vector<double>& dP,
+                           Matrix* dX, std::size_t workers = 0) {
+    require_width(X, layer.n_in, "lmkan_backward");
+    require_width(dY, layer.n_out, "lmkan_backward");
+    if (X.rows() != dY.rows()) throw std::invalid_argument("lmkan_backward: X and dY row counts differ");
+    if (dP.size() != layer.P.size()) throw std::invalid_argument("lmkan_backward: dP size mismatch");
+    if (dX && (dX->rows() != X.rows() || dX->cols() != X.cols())) *dX = Matrix(X.rows(), X.cols());
+    if (workers == 0) workers = worker_count();
+    if (X.rows() == 0) return;
+    lmkan_b200_layer* h = layer.prepared();
+    detail::throw_status(lmkan_b200_backward_host_f64(h, layer.P.data(), X.data(), dY.data(), dP.data(),
+                                                      dX ? dX->data() : nullptr,
+                                                      static_cast<std::int64_t>(X.rows()), workers),
+                         "lmkan_backward");
 }
 
 // A fused pure-lookup model resident on one GPU: what load_model returns for a

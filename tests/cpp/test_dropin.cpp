@@ -180,6 +180,64 @@ static void test_interval_index() {  // test_grid.cpp:108-114
     CHECK(interval_index(g4, std::nan("")) == 0);
 }
 
+// test_layer.cpp:147-226 restated: zero upstream -> zero; compact support of
+// one row; dP against central differences of the fp64 dense oracle (the map
+// is linear in P); bitwise determinism for a fixed worker count.
+static void test_backward() {
+    LmKanLayer layer = init_layer(4, 3, 4, 321);
+    layer.gamma = 0.5;
+    std::mt19937_64 g(13);
+    const Matrix X = random_batch(8, 4, g);
+    std::vector<double> dP(layer.P.size(), 0.0);
+    Matrix dX;
+    lmkan_backward(layer, X, Matrix(8, 3, 0.0), dP, &dX);
+    for (double v : dP) CHECK(v == 0.0);
+    for (std::size_t i = 0; i < dX.size(); ++i) CHECK(dX.data()[i] == 0.0);
+    CHECK(dX.rows() == 8 && dX.cols() == 4);
+
+    LmKanLayer one = init_layer(2, 1, 4, 7);
+    one.gamma = 1.0;
+    Matrix X1(1, 2);
+    X1(0, 0) = 0.2;
+    X1(0, 1) = -0.4;
+    std::vector<double> d1(one.P.size(), 0.0);
+    lmkan_backward(one, X1, Matrix(1, 1, 1.0), d1, nullptr);
+    int nonzero = 0;
+    for (double v : d1) nonzero += v != 0.0;
+    CHECK(nonzero == 4);
+
+    for (int G : {3, 4}) {
+        LmKanLayer L = init_layer(4, 3, G, 1000 + G);
+        L.gamma = 0.7;
+        const Matrix Xg = random_batch(8, 4, g);
+        const Matrix dY = random_batch(8, 3, g);
+        std::vector<double> dPg(L.P.size(), 0.0);
+        lmkan_backward(L, Xg, dY, dPg, nullptr, 3);
+        std::vector<double> again(L.P.size(), 0.0);
+        lmkan_backward(L, Xg, dY, again, nullptr, 3);
+        CHECK(again == dPg);
+        auto loss = [&](const LmKanLayer& l) {
+            const Matrix y = dense_reference(l, Xg);
+            double acc = 0.0;
+            for (std::size_t i = 0; i < y.size(); ++i) acc += y.data()[i] * dY.data()[i];
+            return acc;
+        };
+        const double h = 1e-3;
+        for (std::size_t i = 0; i < L.P.size(); i += 7) {
+            LmKanLayer b = L;
+            b.P[i] += h;
+            const double hi = loss(b);
+            b.P[i] -= 2 * h;
+            const double lo = loss(b);
+            const double fd = (hi - lo) / (2 * h);
+            CHECK(std::abs(dPg[i] - fd) <= 1e-8 * std::max(1.0, std::abs(fd)));
+        }
+    }
+    std::vector<double> bad(3, 0.0);
+    CHECK_THROWS_AS(lmkan_backward(layer, X, Matrix(8, 3), bad, nullptr), std::invalid_argument);
+    CHECK_THROWS_AS(lmkan_backward(layer, X, Matrix(7, 3), dP, nullptr), std::invalid_argument);
+}
+
 // serialize.hpp:185-301 + model.hpp:313-316 on a model the REFERENCE saved
 // (tests/golden/lmk1/pure_f64.lmk1, fuse_model of a relu_first student):
 // model_infer equals the chain of lmkan_forward calls over layers built from
@@ -242,6 +300,7 @@ int main(int argc, char** argv) {
     test_linear_sheets();
     test_determinism_and_cache();
     test_interval_index();
+    test_backward();
     if (argc > 1) test_load_model(argv[1]);
     std::printf("test_dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
