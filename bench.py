@@ -347,10 +347,11 @@ def main():
     launches_per_step = sum(l.plan(B)["launches"] for l in layers)
 
     # ---- e2e through the public API: pinned host input in, host result out.
-    # Single dense layer: the synchronous host entry lmkan_b200_forward_host_f32
-    # (H2D / kernels / D2H pipelined over row chunks inside the library).
-    # Chains and conv: H2D of the input, the device chain, D2H of the final
-    # output, on the bench stream (no overlap), then a host read of the result.
+    # Single dense layer: the synchronous host entry lmkan_b200_forward_host_f32;
+    # chains / tiny batches: lmkan_b200_model_infer_host_f32; conv:
+    # lmkan_b200_conv_forward_host_f32 (each pipelines H2D / kernels / D2H over
+    # row or image chunks on two internal streams). Output-sharded: H2D, the
+    # device step with its all-gather, D2H, then a host read of the result.
     e2e = None
     if not args.no_e2e:
         Xh = X.cpu().pin_memory()
@@ -361,6 +362,9 @@ def main():
         def host_step():
             if model is not None:  # model_infer drop-in: chunked H2D / graph chain / D2H
                 model.infer_host_ptr(Xh.data_ptr(), Yh.data_ptr(), B, np.float32)
+            elif conv and len(layers) == 1:  # host conv entry: image chunks, copies overlapped
+                layers[0].conv_forward_host_ptr(Xh.data_ptr(), conv["N"], conv["H"], conv["W"], conv["C"], conv["k"],
+                                                conv["s"], Yh.data_ptr())
             elif single:
                 layers[0].forward_host_ptr(Xh.data_ptr(), Yh.data_ptr(), B, np.float32)
             else:

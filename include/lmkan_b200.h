@@ -133,6 +133,10 @@ int lmkan_b200_forward_f64(const lmkan_b200_layer* layer, const double* X_dev, d
  * messages as unfold_conv. */
 int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* layer, const float* img_dev, int N, int H,
                                 int W, int C, int k, int s, float* Y_dev, void* stream);
+/* The same conv with host img / Y (synchronous): image chunks alternate over
+ * two internal streams so the copies overlap the kernels. */
+int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* layer, const float* img, int N, int H, int W,
+                                     int C, int k, int s, float* Y, size_t workers);
 /* Drop-in synchronous host paths: X/Y in host memory (pinned or pageable),
  * copies and kernels pipelined over row chunks on internal streams; returns
  * when Y is on the host. `workers` is accepted for signature parity with

@@ -184,6 +184,22 @@ class Layer:
                                               _ptr(Y), _stream_ptr(stream)))
         return Y
 
+    def conv_forward_host(self, img: np.ndarray, k: int, s: int = 1, Y: Optional[np.ndarray] = None) -> np.ndarray:
+        """Host conv (synchronous, copies overlapped with the kernels): img
+        [N, H, W, C] float32 -> Y [N, out_h, out_w, n_out] float32."""
+        img = np.ascontiguousarray(img, np.float32)
+        N, H, W, Cc = img.shape
+        oh, ow = (H - k) // s + 1, (W - k) // s + 1
+        if Y is None:
+            Y = np.empty((N, max(oh, 0), max(ow, 0), self.n_out), np.float32)
+        check(lib.lmkan_b200_conv_forward_host_f32(self._h, _ptr(img), int(N), int(H), int(W), int(Cc), int(k), int(s),
+                                                   _ptr(Y), 0))
+        return Y
+
+    def conv_forward_host_ptr(self, img_ptr: int, N: int, H: int, W: int, Cc: int, k: int, s: int, Y_ptr: int) -> None:
+        check(lib.lmkan_b200_conv_forward_host_f32(self._h, C.c_void_p(img_ptr), int(N), int(H), int(W), int(Cc),
+                                                   int(k), int(s), C.c_void_p(Y_ptr), 0))
+
     def forward(self, X, stream=None):
         """torch CUDA tensor in -> CUDA tensor out; numpy in -> numpy out (host path)."""
         if isinstance(X, np.ndarray):

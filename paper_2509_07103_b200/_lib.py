@@ -40,6 +40,8 @@ _SIGS = [
     ("lmkan_b200_forward_f64", C.c_int, [_P, _P, _P, C.c_int64, _P]),
     ("lmkan_b200_conv_forward_f32", C.c_int,
      [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
+    ("lmkan_b200_conv_forward_host_f32", C.c_int,
+     [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
     ("lmkan_b200_forward_host_f64", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
     ("lmkan_b200_forward_host_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
     ("lmkan_b200_locate_f32", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),

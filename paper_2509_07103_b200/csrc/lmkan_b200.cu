@@ -625,9 +625,10 @@ int lmkan_b200_forward_f32_timed(const lmkan_b200_layer* L, const float* X, floa
     return forward_device<float>(L, X, Y, rows, static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev_begin),
                                  static_cast<cudaEvent_t>(ev_end));
 }
-int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,
-                                int s, float* Y, void* stream) {
-    // argument checks of unfold_conv (conv.hpp:40-45), then the layer width check (layer.hpp:110)
+namespace {
+// argument checks of unfold_conv (conv.hpp:40-45), then the layer width check
+// (layer.hpp:110); fills the implicit-im2col input map.
+int conv_map(const lmkan_b200_layer* L, int N, int H, int W, int C, int k, int s, InputMap& im) {
     if (!L) return fail(LMKAN_B200_EINVAL, "conv_forward: null layer");
     if (k < 1 || s < 1) return fail(LMKAN_B200_EINVAL, "unfold_conv: k and s must be positive");
     if (k > H || k > W) return fail(LMKAN_B200_EINVAL, "unfold_conv: kernel larger than image");
@@ -637,7 +638,7 @@ int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int
     if (static_cast<int64_t>(k) * k * C != L->n_in)
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: expected width " + std::to_string(L->n_in) + ", got " +
                                            std::to_string(static_cast<int64_t>(k) * k * C));
-    InputMap im{};
+    im = InputMap{};
     im.conv = 1;
     im.out_h = (H - k) / s + 1;
     im.out_w = (W - k) / s + 1;
@@ -646,6 +647,65 @@ int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int
     im.C = C;
     im.k = k;
     im.s = s;
+    return LMKAN_B200_OK;
+}
+}  // namespace
+
+// Synchronous host conv: image chunks alternate over two streams so the H2D of
+// chunk c+1 and the D2H of chunk c-1 overlap the kernels of chunk c.
+int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,
+                                     int s, float* Y, size_t /*workers*/) {
+    InputMap im;
+    if (int rc = conv_map(L, N, H, W, C, k, s, im)) return rc;
+    if (N == 0) return LMKAN_B200_OK;
+    if (!img || !Y) return fail(LMKAN_B200_EINVAL, "conv_forward: null image or output");
+    DeviceGuard g(L->device);
+    static thread_local HostStreams hs[64];
+    HostStreams& HS = hs[L->device & 63];
+    for (auto& st : HS.s)
+        if (!st) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const int64_t per_img = static_cast<int64_t>(im.out_h) * im.out_w;
+    Plan pl;
+    if (!make_plan(L, per_img * N, max_smem_optin(L->device), pl))
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
+    // at least one full wave of CTAs per chunk, else ~8 chunks
+    const int64_t min_imgs = (static_cast<int64_t>(pl.sh.R) * kNumSMs / std::max(1, L->n_ot) + per_img - 1) / per_img;
+    const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));
+    const size_t in_img = static_cast<size_t>(H) * W * C, out_img = static_cast<size_t>(per_img) * L->n_out;
+    float* dI[2] = {nullptr, nullptr};
+    float* dY[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dI[i]), sizeof(float) * in_img * chunk, HS.s[i]));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dY[i]), sizeof(float) * out_img * chunk, HS.s[i]));
+    }
+    int rc = LMKAN_B200_OK;
+    int c = 0;
+    for (int n0 = 0; n0 < N && rc == LMKAN_B200_OK; n0 += chunk, ++c) {
+        const int i = c & 1;
+        const int n = std::min(chunk, N - n0);
+        cudaError_t e = cudaMemcpyAsync(dI[i], img + n0 * in_img, sizeof(float) * in_img * n, cudaMemcpyHostToDevice,
+                                        HS.s[i]);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "conv_forward: H2D"); break; }
+        rc = forward_device<float>(L, dI[i], dY[i], per_img * n, HS.s[i], nullptr, nullptr, im);
+        if (rc) break;
+        e = cudaMemcpyAsync(Y + n0 * out_img, dY[i], sizeof(float) * out_img * n, cudaMemcpyDeviceToHost, HS.s[i]);
+        if (e != cudaSuccess) rc = cuda_fail(e, "conv_forward: D2H");
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeAsync(dI[i], HS.s[i]);
+        cudaFreeAsync(dY[i], HS.s[i]);
+    }
+    for (int i = 0; i < 2; ++i) {
+        const cudaError_t e = cudaStreamSynchronize(HS.s[i]);
+        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = cuda_fail(e, "conv_forward: stream sync");
+    }
+    return rc;
+}
+
+int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,
+                                int s, float* Y, void* stream) {
+    InputMap im;
+    if (int rc = conv_map(L, N, H, W, C, k, s, im)) return rc;
     const int64_t rows = static_cast<int64_t>(N) * im.out_h * im.out_w;
     return forward_device<float>(L, img, Y, rows, static_cast<cudaStream_t>(stream), nullptr, nullptr, im);
 }

@@ -383,6 +383,18 @@ def test_conv_implicit_im2col(torch, pkg, oracle, N, H, W, C, k, s, n_out, G):
     assert torch.equal(Y.reshape(-1, n_out), Yx)  # same rows, same kernel, same order
     ref = oracle.forward(G, P.astype(np.float64), patches.astype(np.float64), 1.0)
     assert _mixed(Y.reshape(-1, n_out).cpu().numpy(), ref).max() <= TOL
+    # host entry (image chunks over two streams): same bits as the device call
+    assert np.array_equal(layer.conv_forward_host(img, k, s), Y.cpu().numpy())
+
+
+def test_conv_host_chunked_cfg4_shape(torch, pkg):
+    """cfg4 geometry through the host conv entry (several image chunks) equals
+    the single device launch bitwise."""
+    rng = np.random.default_rng(4)
+    img = rng.standard_normal((300, 34, 34, 16)).astype(np.float32)
+    layer = pkg.Layer.random(144, 16, 16, seed=4)
+    Yd = layer.conv_forward(torch.from_numpy(img).cuda(), 3, 1).cpu().numpy()
+    assert np.array_equal(layer.conv_forward_host(img, 3, 1), Yd)
 
 
 def test_conv_argument_errors(torch, pkg):
