@@ -55,6 +55,18 @@ def fma_per_row(n_in: int, n_out: int) -> int:
     return 2 * n_in * n_out  # costs.hpp:14-23
 
 
+def smem_ceiling(fma_per_row: float, sm_mhz, kernel_ms: float, rows: int) -> dict:
+    """Gather ceiling: 148 SMs x 32 FMA/clk (128 B/clk of shared-memory reads
+    at 4 B per coefficient) at the measured SM clock, in rows/s, and the
+    kernel's fraction of it."""
+    mhz = float(sm_mhz or 1965.0)
+    fma_s = 148 * 32 * mhz * 1e6
+    ceil_rows = fma_s / fma_per_row
+    achieved = rows / (kernel_ms / 1e3)
+    return {"fma_per_s": fma_s, "rows_per_s": ceil_rows, "achieved_rows_per_s": achieved,
+            "frac": achieved / ceil_rows, "sm_mhz": mhz}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -450,7 +462,10 @@ def main():
                                        "the same K steps after the graph-replayed timed region")
                      if model is not None else
                      "CUDA events around each gather kernel on the launch stream, inside the timed region",
-                     "fp32_fma_tflops": fmas / (kernel_ms / 1e3) / 1e12},
+                     "fp32_fma_tflops": fmas / (kernel_ms / 1e3) / 1e12,
+                     # the ceiling that binds the gather: one 4-byte
+                     # coefficient per FMA through the 128 B/clk/SM shared-memory port
+                     "smem_gather_ceiling": smem_ceiling(fmas / B, clocks.get("sm_mhz"), kernel_ms, B)},
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
