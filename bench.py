@@ -232,6 +232,9 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="config 5 under torchrun: all-gather of the output columns fused into the gather "
+                         "kernel's epilogue (NVLink peer stores + device barrier) or a separate NCCL all-gather")
     ap.add_argument("--shards", type=int, default=0,
                     help="config 5: number of output shards (default: world size); with one process, "
                          "measures shard 0 of K (what each of K GPUs computes) without the all-gather")
@@ -259,6 +262,8 @@ def main():
     G = cfg["G"]
     B = cfg["batch"]
     out_sharded = bool(cfg.get("out_sharded"))
+    peers = None
+    Yfull = None
     shards = (args.shards or ws) if out_sharded else 1
     if out_sharded:
         from paper_2509_07103_b200 import sharding
@@ -267,6 +272,9 @@ def main():
         layers = [pkg.Layer.random(n_in0, n_out0, G, seed=1000, gamma=1.0, device=local, out_range=(ob, oe))]
         cfg = dict(cfg, layers=[(n_in0, oe - ob)])  # this rank's local layer
         Yfull = torch.empty((B, n_out0), device=f"cuda:{local}") if ws > 1 else None
+        # all-gather of the column shards: fused into the gather kernel's
+        # epilogue (NVLink stores into every rank's Y + device barrier), or NCCL
+        peers = sharding.PeerGather(B, n_out0, local) if ws > 1 and args.gather == "fused" else None
     else:
         layers = [pkg.Layer.random(n_in, n_out, G, seed=1000 + i, gamma=1.0, device=local)
                   for i, (n_in, n_out) in enumerate(cfg["layers"])]
@@ -312,12 +320,18 @@ def main():
                                  stream=stream)
                 if i is not None:
                     gev[i][li][1].record(stream)
+            elif peers is not None:  # fused: the epilogue writes every rank's full-width Y
+                if i is not None:
+                    gev[i][li][0].record(stream)
+                peers.forward(lay, cur, ob, stream)
+                if i is not None:
+                    gev[i][li][1].record(stream)
             elif i is None:
                 lay.forward_into(cur, out, stream)
             else:
                 lay.forward_into_timed(cur, out, gev[i][li][0], gev[i][li][1], stream)
             cur = out
-        if out_sharded and ws > 1:  # NCCL all-gather of the output-column shards
+        if out_sharded and ws > 1 and peers is None:  # NCCL all-gather of the output-column shards
             sharding.gather_columns(acts[-1], n_out0, ws, rank, align=16, out=Yfull)
 
     for _ in range(args.warmup):
@@ -337,6 +351,8 @@ def main():
     torch.cuda.synchronize()
     if sampler:
         sampler.end()
+    if peers is not None:
+        peers.check()  # no rank timed out at the device barrier
     if model is not None:
         # graph replays carry no per-kernel events: time the gather kernels in
         # an eager pass of the same K steps right after the timed region
@@ -367,7 +383,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         Xh = X.cpu().pin_memory()
-        n_last = cfg["layers"][-1][1]
+        # the step's result: the full gathered Y when output-sharded over ranks
+        Yres = (peers.Y if peers is not None else Yfull) if (out_sharded and ws > 1) else acts[-1]
+        n_last = Yres.shape[1]
         Yh = torch.empty((B, n_last), dtype=torch.float32).pin_memory()
         single = len(layers) == 1 and not conv
 
@@ -383,7 +401,7 @@ def main():
                 Xd = torch.empty_like(X)
                 Xd.copy_(Xh, non_blocking=True)
                 step(src=Xd)
-                Yh.copy_(acts[-1], non_blocking=True)
+                Yh.copy_(Yres, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             return float(Yh[0, 0])  # the step's result read on the host
 
@@ -407,6 +425,8 @@ def main():
                "timer": "host wall clock around H2D + forward + D2H + host read (public API)"}
 
     if rank != 0:
+        if peers is not None:
+            peers.close()
         if dist:
             dist.destroy_process_group()
         return
@@ -446,7 +466,7 @@ def main():
                    "global_batch": B if out_sharded else ws * B,
                    "parallelism": (f"output-sharded over {shards} (this run: {ws} process(es); shard "
                                    f"{rank % shards}, n_out_local={cfg['layers'][0][1]}"
-                                   f"{', NCCL all-gather of Y columns' if ws > 1 else ', no all-gather: single-rank shard measurement'})"
+                                   f"{(', all-gather of Y columns fused into the epilogue (NVLink peer stores)' if args.gather == 'fused' else ', NCCL all-gather of Y columns') if ws > 1 else ', no all-gather: single-rank shard measurement'})"
                                    if out_sharded else f"dp{ws} (batch rows, no collective)"),
                    "l2": "inputs larger than L2: X %.0f MB, table %.0f MB vs 126 MB L2" % (
                        B * cfg["layers"][0][0] * 4 / 1e6, sum(l.table_bytes for l in layers) / 1e6),
@@ -473,6 +493,8 @@ def main():
         "impl": "b200",
     }
     print(json.dumps(out))
+    if peers is not None:
+        peers.close()
     if dist:
         dist.destroy_process_group()
 

@@ -137,6 +137,35 @@ int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* layer, const float* img_
  * two internal streams so the copies overlap the kernels. */
 int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* layer, const float* img, int N, int H, int W,
                                      int C, int k, int s, float* Y, size_t workers);
+/* ---- output-sharded layers: the all-gather fused into the epilogue ----
+ *
+ * Forward writing the layer's (local) output columns into n_dest (1..8)
+ * row-major fp32 buffers dests[d][r * ld + col0 + q]: on a GPU of an
+ * output-sharded layer the destinations are the
+ * full-width Y of every rank — its own and the peers', mapped over NVLink with
+ * lmkan_b200_ipc_open_handle — so each CTA's tile reaches every GPU as NVLink
+ * stores while the other CTAs are still gathering (no separate collective).
+ * col0 = the shard's first column, ld = the full width. */
+int lmkan_b200_forward_f32_dests(const lmkan_b200_layer* layer, const float* X_dev, float* const* dests,
+                                 int n_dest, int64_t ld, int col0, int64_t rows, void* stream);
+/* CUDA IPC plumbing for the peer destinations: the 64-byte handle
+ * (cudaIpcMemHandle_t) of the allocation containing dev_ptr plus dev_ptr's
+ * offset inside it (a caching allocator hands out pieces of larger segments);
+ * opened in another process on `device` (peer access enabled lazily) as
+ * base + offset; closed with the pointer open returned. */
+int lmkan_b200_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+int lmkan_b200_ipc_open_handle(const void* handle, uint64_t offset, int device, void** dev_ptr);
+int lmkan_b200_ipc_close(void* dev_ptr);
+/* Device-side barrier after the fused gather, on the same stream: rank
+ * `rank` of `world` (<= 8) stores `epoch` (> 0, increasing) into slot `rank`
+ * of every rank's int32[world] flag array (flag_arrays[q], IPC-mapped;
+ * system-scope release after a system fence) and spins until all slots of its
+ * own array reach `epoch` (acquire). status_dev (int32, device) is set to
+ * 1 + q if peer q did not arrive within timeout_ms (<= 0: 10 s), else left
+ * unchanged. */
+int lmkan_b200_peer_barrier(int* const* flag_arrays, int world, int rank, int epoch, int timeout_ms,
+                            int* status_dev, void* stream);
+
 /* Drop-in synchronous host paths: X/Y in host memory (pinned or pageable),
  * copies and kernels pipelined over row chunks on internal streams; returns
  * when Y is on the host. `workers` is accepted for signature parity with

@@ -165,6 +165,16 @@ class Layer:
         fn = lib.lmkan_b200_forward_f32 if X.dtype == torch.float32 else lib.lmkan_b200_forward_f64
         check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream)))
 
+    def forward_dests(self, X, dest_ptrs, ld: int, col0: int, stream=None) -> None:
+        """Forward (float32) storing this layer's output columns into every
+        destination buffer: dest[r * ld + col0 + q] (device pointers, e.g. the
+        full-width Y of every GPU of an output-sharded layer)."""
+        if X.dim() != 2 or X.shape[1] != self.n_in:
+            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
+        arr = (C.c_void_p * len(dest_ptrs))(*[int(p) for p in dest_ptrs])
+        check(lib.lmkan_b200_forward_f32_dests(self._h, _ptr(X), arr, len(dest_ptrs), int(ld), int(col0),
+                                               int(X.shape[0]), _stream_ptr(stream)))
+
     def forward_into_timed(self, X, Y, ev_begin, ev_end, stream=None) -> None:
         """forward_into (float32) recording torch.cuda.Events around the gather kernel."""
         check(lib.lmkan_b200_forward_f32_timed(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream),
@@ -306,6 +316,38 @@ class Layer:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# Peer memory for the fused output all-gather (sharding.PeerGather uses these).
+
+def ipc_handle(t) -> Tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding CUDA tensor `t`,
+    offset of t's data inside that allocation)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    check(lib.lmkan_b200_ipc_get_handle(C.c_void_p(t.data_ptr()), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int, device: int) -> int:
+    """Map a peer's allocation (from ipc_handle in another process); returns
+    the device pointer of the peer tensor's data."""
+    p = C.c_void_p()
+    check(lib.lmkan_b200_ipc_open_handle(C.create_string_buffer(bytes(handle), 64), int(offset), int(device),
+                                         C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib.lmkan_b200_ipc_close(C.c_void_p(ptr)))
+
+
+def peer_barrier(flag_ptrs, rank: int, epoch: int, status, timeout_ms: int = 10000, stream=None) -> None:
+    """Enqueue the device-side barrier (see include/lmkan_b200.h)."""
+    arr = (C.c_void_p * len(flag_ptrs))(*[int(p) for p in flag_ptrs])
+    check(lib.lmkan_b200_peer_barrier(arr, len(flag_ptrs), int(rank), int(epoch), int(timeout_ms),
+                                      C.c_void_p(status.data_ptr()), _stream_ptr(stream)))
 
 
 # ---------------------------------------------------------------------------

@@ -38,6 +38,11 @@ _SIGS = [
     ("lmkan_b200_forward_f32", C.c_int, [_P, _P, _P, C.c_int64, _P]),
     ("lmkan_b200_forward_f32_timed", C.c_int, [_P, _P, _P, C.c_int64, _P, _P, _P]),
     ("lmkan_b200_forward_f64", C.c_int, [_P, _P, _P, C.c_int64, _P]),
+    ("lmkan_b200_forward_f32_dests", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int64, C.c_int, C.c_int64, _P]),
+    ("lmkan_b200_ipc_get_handle", C.c_int, [_P, _P, C.POINTER(C.c_uint64)]),
+    ("lmkan_b200_ipc_open_handle", C.c_int, [_P, C.c_uint64, C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_ipc_close", C.c_int, [_P]),
+    ("lmkan_b200_peer_barrier", C.c_int, [C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("lmkan_b200_conv_forward_f32", C.c_int,
      [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("lmkan_b200_conv_forward_host_f32", C.c_int,

@@ -66,6 +66,34 @@ __host__ __device__ inline int in_coloff(const InputMap& m, int col) {
     return (dy * m.W + dx) * m.C + ch;
 }
 
+// Where the layer output y[r][q] (local column q) goes: n row-major buffers
+// base[d][r * ld + col0 + q]. The plain forward has one (Y, ld = n_out,
+// col0 = 0); an output-sharded layer can write its columns straight into the
+// full-width Y of every GPU (peer pointers mapped over NVLink), which fuses the
+// all-gather of the shards into the gather kernel's epilogue.
+constexpr int kMaxDest = 8;
+template <typename XT>
+struct OutDests {
+    XT* base[kMaxDest];
+    int64_t ld;
+    int col0;
+    int n;
+};
+template <typename XT>
+__host__ __device__ inline OutDests<XT> single_dest(XT* Y, int n_out) {
+    OutDests<XT> o{};
+    o.base[0] = Y;
+    o.ld = n_out;
+    o.col0 = 0;
+    o.n = 1;
+    return o;
+}
+template <typename XT>
+__host__ __device__ inline OutDests<XT> dests_at_row(OutDests<XT> o, int64_t r0) {
+    for (int d = 0; d < o.n && d < kMaxDest; ++d) o.base[d] += r0 * o.ld;
+    return o;
+}
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -472,7 +500,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
 template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
-    fwd_fused_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
+    fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im) {
@@ -699,24 +727,34 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     }
 
-    // epilogue: y *= gamma (layer.hpp:131), masked store of the warp's rows
+    // epilogue: y *= gamma (layer.hpp:131), masked store of the warp's rows into
+    // every destination (peer destinations are NVLink stores issued as the
+    // CTA's tile completes, overlapping the other CTAs' gathers)
     const int col = ot * OT + 4 * c4;
-    const bool y_vec_ok = (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (n_out & 3) == 0;
 #pragma unroll
-    for (int j = 0; j < RT; ++j) {
-        const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
-        if (r >= rows) continue;
-        const float v[4] = {acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma, acc[j].w * gamma};
-        XT* yr = Y + r * n_out;
-        if constexpr (sizeof(XT) == 4) {
-            if (col + 3 < n_out && y_vec_ok) {
-                *reinterpret_cast<float4*>(yr + col) = make_float4(v[0], v[1], v[2], v[3]);
-                continue;
+    for (int j = 0; j < RT; ++j) acc[j] = make_float4(acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma,
+                                                      acc[j].w * gamma);
+#pragma unroll
+    for (int d = 0; d < kMaxDest; ++d) {  // unrolled: constant indices keep `out` in the parameter space
+        if (d >= out.n) break;
+        XT* const base = out.base[d] + out.col0;
+        const bool y_vec_ok = (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (out.ld & 3) == 0;
+#pragma unroll
+        for (int j = 0; j < RT; ++j) {
+            const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
+            if (r >= rows) continue;
+            XT* yr = base + r * out.ld;
+            if constexpr (sizeof(XT) == 4) {
+                if (col + 3 < n_out && y_vec_ok) {
+                    *reinterpret_cast<float4*>(yr + col) = acc[j];
+                    continue;
+                }
             }
-        }
+            const float v[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (col + e < n_out) yr[col + e] = static_cast<XT>(v[e]);
+            for (int e = 0; e < 4; ++e)
+                if (col + e < n_out) yr[col + e] = static_cast<XT>(v[e]);
+        }
     }
 }
 
@@ -738,7 +776,7 @@ __host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) 
 
 template <typename XT, int NO>
 __global__ void __launch_bounds__(kNarrowThreads, 1)
-    narrow_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
+    narrow_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                   const float* __restrict__ table, float gamma, const __grid_constant__ GridConst gc,
                   const InputMap im) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -798,10 +836,14 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
             }
         }
         for (; p < pairs; ++p) one_pair(p, xr[in_coloff(im, 2 * p)], xr[in_coloff(im, 2 * p + 1)]);
-        XT* yr = Y + r * n_out;
 #pragma unroll
-        for (int q = 0; q < NO; ++q)
-            if (q < n_out) yr[q] = static_cast<XT>(acc[q] * gamma);
+        for (int d = 0; d < kMaxDest; ++d) {
+            if (d >= out.n) break;
+            XT* yr = out.base[d] + out.col0 + r * out.ld;
+#pragma unroll
+            for (int q = 0; q < NO; ++q)
+                if (q < n_out) yr[q] = static_cast<XT>(acc[q] * gamma);
+        }
     }
 }
 

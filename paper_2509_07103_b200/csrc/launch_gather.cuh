@@ -7,7 +7,7 @@
 namespace lmkan_b200 {
 
 template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps>
-cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                            const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
@@ -24,7 +24,7 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
 }
 
 template <int OT, typename XT, int MODE, bool SLAB>
-cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                             const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT = 4) so the grid still spans the GPU
         switch (pl.sh.NW) {
@@ -43,7 +43,7 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
 }
 
 template <int OT, typename XT>
-cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                               const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
     if (pl.mode == kModeGlobal)
         return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, st);
@@ -58,10 +58,12 @@ cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X
 
 #define LMKAN_B200_INSTANTIATE_GATHER(OT)                                                                        \
     template cudaError_t lmkan_b200::launch_gather<OT, float>(const lmkan_b200_layer*, const lmkan_b200::Plan&, \
-                                                              const float*, float*, int64_t, const float2*,      \
+                                                              const float*, const lmkan_b200::OutDests<float>&, \
+                                                              int64_t, const float2*,                            \
                                                               const int*, const lmkan_b200::InputMap&,           \
                                                               cudaStream_t);                                     \
     template cudaError_t lmkan_b200::launch_gather<OT, double>(const lmkan_b200_layer*,                          \
-                                                               const lmkan_b200::Plan&, const double*, double*,  \
+                                                               const lmkan_b200::Plan&, const double*,           \
+                                                               const lmkan_b200::OutDests<double>&,              \
                                                                int64_t, const float2*, const int*,               \
                                                                const lmkan_b200::InputMap&, cudaStream_t);

@@ -34,7 +34,7 @@ struct Plan {
 // Launch the gather kernel variant selected by `pl` for output tile OT
 // (definitions in launch_gather.cuh, instantiated in gather_ot{16,32,64}.cu).
 template <int OT, typename XT>
-cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                           const float2* recW, const int* recO, const InputMap& im, cudaStream_t st);
 
 // Entry points shared with the other host translation units (model.cu):

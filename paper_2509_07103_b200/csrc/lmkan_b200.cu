@@ -197,7 +197,7 @@ size_t record_scratch_cap() { return static_cast<size_t>(env_int("LMKAN_B200_MAX
 
 // One launch group (K1 + K2 in staged mode, K3 otherwise) over `rows` rows.
 template <typename XT, int NO>
-cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows,
+cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                           const InputMap& im, cudaStream_t st) {
     static int configured[64] = {0};
     if (!configured[L->device & 63]) {
@@ -212,7 +212,8 @@ cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X
 }
 
 template <typename XT>
-int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, int64_t rows, const InputMap& im,
+int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
+                 const InputMap& im,
                  cudaStream_t st, cudaEvent_t ev_begin, cudaEvent_t ev_end) {
     if (pl.mode == kModeNarrow) {
         if (ev_begin) cudaEventRecord(ev_begin, st);
@@ -263,14 +264,20 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, XT* Y, 
 }
 
 template <typename XT>
-int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
-                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, InputMap im = InputMap{}) {
+int forward_device_dests(const lmkan_b200_layer* L, const XT* X, const OutDests<XT>& out, int64_t rows,
+                         cudaStream_t st, cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr,
+                         InputMap im = InputMap{}) {
     if (!L) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null layer");
     if (rows < 0) return fail(LMKAN_B200_EINVAL, "lmkan_forward: negative row count");
     if (rows == 0) return LMKAN_B200_OK;
-    if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
-    if (reinterpret_cast<uintptr_t>(Y) % sizeof(XT) != 0 || reinterpret_cast<uintptr_t>(X) % sizeof(XT) != 0)
+    if (!X || out.n < 1 || out.n > kMaxDest) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
+    for (int d = 0; d < out.n; ++d)
+        if (!out.base[d] || reinterpret_cast<uintptr_t>(out.base[d]) % sizeof(XT) != 0)
+            return fail(LMKAN_B200_EINVAL, "lmkan_forward: X and Y must be aligned to their element size");
+    if (reinterpret_cast<uintptr_t>(X) % sizeof(XT) != 0)
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: X and Y must be aligned to their element size");
+    if (out.col0 < 0 || out.ld < out.col0 + L->n_out)
+        return fail(LMKAN_B200_EINVAL, "lmkan_forward: output row stride narrower than the layer's columns");
     DeviceGuard g(L->device);
     const int cap = max_smem_optin(L->device);
     Plan pl;
@@ -292,11 +299,18 @@ int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, 
         const bool first = r0 == 0, last = r0 + n >= rows;
         InputMap imc = im;
         imc.row_offset = r0;
-        if (int rc = forward_rows<XT>(L, pc, X, Y + r0 * L->n_out, n, imc, st, first ? ev_begin : nullptr,
+        if (int rc = forward_rows<XT>(L, pc, X, dests_at_row(out, r0), n, imc, st, first ? ev_begin : nullptr,
                                       last ? ev_end : nullptr))
             return rc;
     }
     return LMKAN_B200_OK;
+}
+
+template <typename XT>
+int forward_device(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st,
+                   cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr, InputMap im = InputMap{}) {
+    if (L && rows > 0 && !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
+    return forward_device_dests<XT>(L, X, single_dest<XT>(Y, L ? L->n_out : 0), rows, st, ev_begin, ev_end, im);
 }
 
 template <typename XT>
@@ -708,6 +722,73 @@ int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int
     if (int rc = conv_map(L, N, H, W, C, k, s, im)) return rc;
     const int64_t rows = static_cast<int64_t>(N) * im.out_h * im.out_w;
     return forward_device<float>(L, img, Y, rows, static_cast<cudaStream_t>(stream), nullptr, nullptr, im);
+}
+int lmkan_b200_forward_f32_dests(const lmkan_b200_layer* L, const float* X, float* const* dests, int n_dest,
+                                 int64_t ld, int col0, int64_t rows, void* stream) {
+    if (!dests || n_dest < 1 || n_dest > kMaxDest)
+        return fail(LMKAN_B200_EINVAL, "forward_dests: 1 to 8 destinations required");
+    OutDests<float> out{};
+    for (int d = 0; d < n_dest; ++d) out.base[d] = dests[d];
+    out.n = n_dest;
+    out.ld = ld;
+    out.col0 = col0;
+    return forward_device_dests<float>(L, X, out, rows, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return fail(LMKAN_B200_EINVAL, "ipc_get_handle: null argument");
+    // the handle names the whole allocation (e.g. a caching-allocator segment):
+    // report the pointer's offset inside it (cuMemGetAddressRange via the
+    // runtime's driver entry point, no libcuda link)
+    using AddrRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static AddrRange range = nullptr;
+    if (!range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(LMKAN_B200_ECUDA, "ipc_get_handle: cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<AddrRange>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+        return fail(LMKAN_B200_ECUDA, "ipc_get_handle: pointer is not a device allocation");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+    return LMKAN_B200_OK;
+}
+namespace {
+std::mutex g_ipc_mu;
+std::vector<std::pair<void*, void*>> g_ipc_open;  // (returned pointer, mapped base)
+}  // namespace
+int lmkan_b200_ipc_open_handle(const void* handle, uint64_t offset, int device, void** dev_ptr) {
+    if (!handle || !dev_ptr) return fail(LMKAN_B200_EINVAL, "ipc_open_handle: null argument");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<char*>(base) + offset;
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    g_ipc_open.emplace_back(*dev_ptr, base);
+    return LMKAN_B200_OK;
+}
+int lmkan_b200_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return LMKAN_B200_OK;
+    void* base = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_ipc_mu);
+        for (auto it = g_ipc_open.begin(); it != g_ipc_open.end(); ++it)
+            if (it->first == dev_ptr) {
+                base = it->second;
+                g_ipc_open.erase(it);
+                break;
+            }
+    }
+    if (!base) return fail(LMKAN_B200_EINVAL, "ipc_close: pointer was not opened by ipc_open_handle");
+    CK(cudaIpcCloseMemHandle(base));
+    return LMKAN_B200_OK;
 }
 int lmkan_b200_forward_f64(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, void* stream) {
     return forward_device<double>(L, X, Y, rows, static_cast<cudaStream_t>(stream));

@@ -7,9 +7,11 @@ Rows of a forward are independent (layer.hpp:118-132) and so are outputs
   own contiguous row shard — no communication at all;
 * output sharding (config 5, tables too large to replicate): every rank holds
   the table columns of one contiguous output block and computes Y[:, block]
-  for all rows; the column blocks are then all-gathered (NCCL over NVLink on
-  B200, gloo in the CPU tests), pipelined over row chunks so the exchange of
-  chunk i overlaps the kernel of chunk i+1.
+  for all rows. The column blocks reach every rank either through the fused
+  path (PeerGather: the gather kernel's epilogue stores each tile straight
+  into every GPU's full-width Y over NVLink, then a device-side flag barrier)
+  or through a collective (gather_columns: NCCL all-gather over NVLink on
+  B200, gloo in the CPU tests, optionally pipelined over row chunks).
 
 Both give results bitwise equal to a single-GPU forward (the per-(row, output)
 summation order does not depend on the partition).
@@ -84,3 +86,71 @@ def output_sharded_forward(compute: Callable, X, n_out: int, world: int, rank: i
         torch.cuda.current_stream().wait_stream(comm_stream)
     del pending
     return Y
+
+
+class PeerGather:
+    """Full-width output buffer shared by all ranks of an output-sharded layer.
+
+    Every rank allocates Y [rows, n_out] and an int32 flag array, publishes
+    CUDA IPC handles (all_gather_object), and maps the peers' buffers. Then
+    ``forward(layer, X, col0)`` runs the rank's shard with the library's
+    multi-destination epilogue (lmkan_b200_forward_f32_dests: the tile of
+    every CTA is stored into all ranks' Y over NVLink as it completes) followed
+    by lmkan_b200_peer_barrier on the same stream, after which Y holds every
+    rank's columns on every GPU — the all-gather fused into the compute, no
+    separate collective. Device pointers only; ranks must be GPUs of one node.
+    """
+
+    def __init__(self, rows: int, n_out: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import paper_2509_07103_b200 as pkg
+        self._pkg = pkg
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 8:
+            raise ValueError("PeerGather: at most 8 ranks (one NVLink domain)")
+        self.device = device
+        self.n_out = n_out
+        self.Y = torch.empty((rows, n_out), dtype=torch.float32, device=f"cuda:{device}")
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device=f"cuda:{device}")
+        self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
+        mine = (pkg.ipc_handle(self.Y), pkg.ipc_handle(self.flags))
+        everyone = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(everyone, mine, group=group)
+        else:
+            everyone = [mine]
+        self._opened: List[int] = []
+        self.y_ptrs, self.flag_ptrs = [], []
+        for q, ((hy, oy), (hf, of)) in enumerate(everyone):
+            if q == self.rank:
+                self.y_ptrs.append(self.Y.data_ptr())
+                self.flag_ptrs.append(self.flags.data_ptr())
+            else:
+                py, pf = pkg.ipc_open(hy, oy, device), pkg.ipc_open(hf, of, device)
+                self._opened += [py, pf]
+                self.y_ptrs.append(py)
+                self.flag_ptrs.append(pf)
+        self.epoch = 0
+        if self.world > 1:
+            dist.barrier(group=group)  # every mapping exists before anyone stores into it
+
+    def forward(self, layer, X, col0: int, stream=None):
+        """This rank's columns [col0, col0 + layer.n_out) into every rank's Y,
+        then the device-side barrier; returns the (full) local Y."""
+        layer.forward_dests(X, self.y_ptrs, self.n_out, col0, stream)
+        self.epoch += 1
+        self._pkg.peer_barrier(self.flag_ptrs, self.rank, self.epoch, self.status, stream=stream)
+        return self.Y
+
+    def check(self) -> None:
+        """Raise if a barrier timed out (call after synchronizing the stream)."""
+        st = int(self.status.item())
+        if st:
+            raise RuntimeError(f"PeerGather: rank {st - 1} did not arrive at the barrier")
+
+    def close(self) -> None:
+        for p in self._opened:
+            self._pkg.ipc_close(p)
+        self._opened = []
