@@ -57,7 +57,8 @@ def main():
         for m in ("staged", "fused") for rt in ("16", "8") for nb in ("2", "1", "3")]
     G, B = cfg["G"], cfg["batch"]
     X = torch.randn((B, cfg["layers"][0][0]), device="cuda")
-    acts = [torch.empty((B, o), device="cuda") for _, o in cfg["layers"]]
+    shard = int(os.environ.get("SWEEP_SHARD", "0"))
+    acts = [torch.empty((B, o // shard if shard else o), device="cuda") for _, o in cfg["layers"]]
     ot_cache = {}
     for v in variants:
         for k in [k for k in os.environ if k.startswith("LMKAN_B200_")]:
@@ -65,7 +66,11 @@ def main():
         os.environ.update(v)
         key = v.get("LMKAN_B200_OT", "")
         if key not in ot_cache:
-            ot_cache[key] = [pkg.Layer.random(a, b, G, seed=1000 + i) for i, (a, b) in enumerate(cfg["layers"])]
+            shard = int(os.environ.get("SWEEP_SHARD", "0"))  # output-sharded layer: shard 0 of SWEEP_SHARD
+            ot_cache.clear()
+            ot_cache[key] = [pkg.Layer.random(a, b, G, seed=1000 + i,
+                                              out_range=(0, b // shard) if shard else None)
+                             for i, (a, b) in enumerate(cfg["layers"])]
         layers = ot_cache[key]
         try:
             ms = time_layer(layers, X, acts)
