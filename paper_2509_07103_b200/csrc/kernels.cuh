@@ -708,6 +708,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 if (atomicAdd(&cnt[slot], 1u) == NW - 1) {  // last warp out refills the slot
                     cnt[slot] = 0;
                     if (u + nbuf < units) {
+                        // acquire side of the counter: every warp's reads of the slot (fenced
+                        // before its increment) happen before the async-proxy overwrite
+                        __threadfence_block();
                         fence_proxy_async();
                         issue(u + nbuf);
                     }
