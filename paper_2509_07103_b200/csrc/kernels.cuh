@@ -347,6 +347,25 @@ __host__ __device__ inline int offset_slot(const ShapeRT& s, int qc) {
     return (warp * s.RPW + sub) * s.OSTRIDE + j;
 }
 
+// Fused chain (model_infer of a fused model, model.hpp:268-315): the NEXT
+// layer's cell records written by this layer's epilogue. Its 4 consecutive
+// outputs per lane are two input pairs of the next layer, located right there
+// (next layer's grid, gc_next) and stored in the next layer's K2 order, so
+// the activation never round-trips through HBM and the next K1 is skipped.
+// Shared memory the emitting epilogue needs (one pass: OT/4 pairs x R rows).
+// + the next layer's grid constants (thresholds, points, inverse widths), so the
+// locates read shared memory instead of divergent parameter-space loads.
+__host__ __device__ inline uint32_t emit_smem_bytes(int OT, int R) {
+    return static_cast<uint32_t>(OT / 4) * R * 12u + kMaxThr * 4u + (kMaxThr + 1) * 8u + kMaxThr * 8u + 16u;
+}
+struct EmitRecords {
+    float2* W;  // [pairs'][rows_pad'] {alpha, gamma}; nullptr: no emission
+    int* O;     // [pairs'][tiles'][OBLK'] packed offsets
+    ShapeRT sh;  // next layer's K2 row shape
+    int64_t rows_pad, tiles;
+    int H;  // next layer's slab height
+};
+
 // Record-ring depth of the staged mode: records of pair p arrive with its first
 // slab and must outlive its S slabs while up to NBUF units are in flight.
 __host__ __device__ inline int staged_nrec(int nbuf, int S) { return (nbuf - 1 + S - 1) / S + 1; }
@@ -503,7 +522,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
-                     const int* __restrict__ recO, int64_t rows_pad, const InputMap im) {
+                     const int* __restrict__ recO, int64_t rows_pad, const InputMap im, const EmitRecords emit,
+                     const __grid_constant__ GridConst gc_next) {
     using Sh = FusedShape<OT, RT, NW>;
     constexpr int R = Sh::R;
     constexpr int NT = NW * 32;
@@ -737,6 +757,81 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
     for (int j = 0; j < RT; ++j) acc[j] = make_float4(acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma,
                                                       acc[j].w * gamma);
+    if constexpr (sizeof(XT) == 4) {
+        if (emit.W) {
+            // fused chain: this lane's outputs col..col+3 are the next layer's pairs
+            // col/2 and col/2 + 1. Two passes (h = 0, 1), one next-layer pair per lane
+            // each: locate into shared memory [pair][row], then coalesced record
+            // stores — rows run contiguously in W, and when both layers use the same
+            // row tile the CTA's offset block of each pair is written whole.
+            constexpr int PP = OT / 4;  // next-layer pairs per pass
+            float2* sW = reinterpret_cast<float2*>(smem);
+            int* sO = reinterpret_cast<int*>(smem + static_cast<size_t>(PP) * R * sizeof(float2));
+            unsigned char* gbase = smem + static_cast<size_t>(PP) * R * 12u;
+            double* npts = reinterpret_cast<double*>(gbase);
+            double* ninv = npts + kMaxThr + 1;
+            float* nthr = reinterpret_cast<float*>(ninv + kMaxThr);
+            const int pn_base = (ot * OT) >> 1;
+            const int pairs_next = n_out >> 1;
+            const bool same_tile = emit.sh.R == R;
+            __syncthreads();  // all warps past the gather loop: the ring space is free
+            for (int k = tid; k < kMaxThr + 1; k += NT) {
+                npts[k] = gc_next.points[k];
+                if (k < kMaxThr) {
+                    ninv[k] = gc_next.inv_h[k];
+                    nthr[k] = gc_next.t32[k];
+                }
+            }
+            for (int h = 0; h < 2; ++h) {
+                __syncthreads();  // grid constants in place / the previous pass's stores done
+#pragma unroll
+                for (int j = 0; j < RT; ++j) {
+                    const int rl = warp * Sh::ROWS_W + j * Sh::RPW + sub;
+                    const int64_t r = row0 + rl;
+                    float2 ag = make_float2(0.f, 0.f);
+                    int packed = 0;
+                    if (r < rows && col + 2 * h + 1 < n_out) {
+                        const float a = h ? acc[j].z : acc[j].x, b = h ? acc[j].w : acc[j].y;
+                        packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.OT, emit.H, ag);
+                    }
+                    sW[c4 * R + rl] = ag;
+                    sO[c4 * R + rl] = packed;
+                }
+                __syncthreads();
+                for (int idx = tid; idx < PP * R; idx += NT) {
+                    const int pl = idx / R, rl = idx - pl * R;
+                    const int pn = pn_base + 2 * pl + h;
+                    const int64_t r = row0 + rl;
+                    if (pn < pairs_next && r < emit.rows_pad) emit.W[static_cast<size_t>(pn) * emit.rows_pad + r] = sW[idx];
+                }
+                if (same_tile) {  // the whole offset block of (pair, tile), slot order, padding slots zeroed
+                    const int ob = emit.sh.OBLK;
+                    for (int idx = tid; idx < PP * ob; idx += NT) {
+                        const int pl = idx / ob, sl = idx - pl * ob;
+                        const int pn = pn_base + 2 * pl + h;
+                        if (pn >= pairs_next) continue;
+                        const int grp = sl / emit.sh.OSTRIDE, jj = sl - grp * emit.sh.OSTRIDE;
+                        int v = 0;
+                        if (jj < emit.sh.RT) {
+                            const int q = (grp / emit.sh.RPW) * emit.sh.ROWS_W + jj * emit.sh.RPW + grp % emit.sh.RPW;
+                            v = sO[pl * R + q];
+                        }
+                        emit.O[(static_cast<size_t>(pn) * emit.tiles + tile) * ob + sl] = v;
+                    }
+                } else {
+                    for (int idx = tid; idx < PP * R; idx += NT) {
+                        const int pl = idx / R, rl = idx - pl * R;
+                        const int pn = pn_base + 2 * pl + h;
+                        const int64_t r = row0 + rl;
+                        if (pn >= pairs_next || r >= emit.rows_pad) continue;
+                        const int slot = offset_slot(emit.sh, static_cast<int>(r & (emit.sh.R - 1)));
+                        emit.O[(static_cast<size_t>(pn) * emit.tiles + (r >> emit.sh.lgR)) * emit.sh.OBLK + slot] =
+                            sO[idx];
+                    }
+                }
+            }
+        }
+    }
 #pragma unroll
     for (int d = 0; d < kMaxDest; ++d) {  // unrolled: constant indices keep `out` in the parameter space
         if (d >= out.n) break;

@@ -8,7 +8,8 @@ namespace lmkan_b200 {
 
 template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
-                           const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
+                           const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
+                           const GridConst* gc_next, cudaStream_t st) {
     auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
@@ -19,39 +20,42 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
     }
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
     kern<<<grid, NW * 32, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
-                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im);
+                                           static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im, emit,
+                                           emit.W ? *gc_next : L->gc);
     return cudaGetLastError();
 }
 
 template <int OT, typename XT, int MODE, bool SLAB>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
-                            const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
+                            const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
+                           const GridConst* gc_next, cudaStream_t st) {
     if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT = 4) so the grid still spans the GPU
         switch (pl.sh.NW) {
-            case 8: return launch_fused_t<OT, 4, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, st);
-            case 4: return launch_fused_t<OT, 4, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, st);
-            case 2: return launch_fused_t<OT, 4, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, st);
-            case 1: return launch_fused_t<OT, 4, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, st);
+            case 8: return launch_fused_t<OT, 4, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 4: return launch_fused_t<OT, 4, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 2: return launch_fused_t<OT, 4, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 1: return launch_fused_t<OT, 4, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
             default: break;
         }
     }
     switch (pl.RT) {
-        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
-        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
-        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, st);
+        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
     }
 }
 
 template <int OT, typename XT>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
-                              const float2* recW, const int* recO, const InputMap& im, cudaStream_t st) {
+                              const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
+                           const GridConst* gc_next, cudaStream_t st) {
     if (pl.mode == kModeGlobal)
-        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, st);
+        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
     if (pl.mode == kModeStaged)
-        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, st)
-                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, st);
-    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, im, st)
-                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, im, st);
+        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
+                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
+                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
 }
 
 }  // namespace lmkan_b200
@@ -61,9 +65,12 @@ cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X
                                                               const float*, const lmkan_b200::OutDests<float>&, \
                                                               int64_t, const float2*,                            \
                                                               const int*, const lmkan_b200::InputMap&,           \
-                                                              cudaStream_t);                                     \
+                                                              const lmkan_b200::EmitRecords&,                    \
+                                                              const lmkan_b200::GridConst*, cudaStream_t);       \
     template cudaError_t lmkan_b200::launch_gather<OT, double>(const lmkan_b200_layer*,                          \
                                                                const lmkan_b200::Plan&, const double*,           \
                                                                const lmkan_b200::OutDests<double>&,              \
                                                                int64_t, const float2*, const int*,               \
-                                                               const lmkan_b200::InputMap&, cudaStream_t);
+                                                               const lmkan_b200::InputMap&,                      \
+                                                               const lmkan_b200::EmitRecords&,                   \
+                                                               const lmkan_b200::GridConst*, cudaStream_t);

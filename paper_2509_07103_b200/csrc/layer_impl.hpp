@@ -35,7 +35,8 @@ struct Plan {
 // (definitions in launch_gather.cuh, instantiated in gather_ot{16,32,64}.cu).
 template <int OT, typename XT>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
-                          const float2* recW, const int* recO, const InputMap& im, cudaStream_t st);
+                          const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
+                          const GridConst* gc_next, cudaStream_t st);
 
 // Entry points shared with the other host translation units (model.cu):
 // defined in lmkan_b200.cu next to the layer C-ABI.
@@ -47,6 +48,10 @@ int cuda_error(cudaError_t e, const char* what);  // maps a CUDA error to a stat
 int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,
                 lmkan_b200_layer** out);
 int forward_device(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, cudaStream_t st);
+// model_infer chain of full layers, fp32, activations through acts[2] except
+// where a layer's epilogue emits the next layer's cell records (fused chain).
+int forward_chain_f32(const lmkan_b200_layer* const* layers, int n, const float* X, float* Y, int64_t rows,
+                      void* const* acts, cudaStream_t st);
 int forward_device(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st);
 }  // namespace api
 

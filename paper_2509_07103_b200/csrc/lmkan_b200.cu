@@ -211,10 +211,20 @@ cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X
     return cudaGetLastError();
 }
 
+// Records handed between the layers of a fused chain: `pre` (the records this
+// layer would otherwise compute in K1) and `emit` (the next layer's records,
+// written by this layer's epilogue).
+struct ChainLink {
+    const float2* preW = nullptr;
+    const int* preO = nullptr;
+    EmitRecords emit{};
+    const GridConst* gc_next = nullptr;
+};
+
 template <typename XT>
 int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                  const InputMap& im,
-                 cudaStream_t st, cudaEvent_t ev_begin, cudaEvent_t ev_end) {
+                 cudaStream_t st, cudaEvent_t ev_begin, cudaEvent_t ev_end, const ChainLink& link = ChainLink{}) {
     if (pl.mode == kModeNarrow) {
         if (ev_begin) cudaEventRecord(ev_begin, st);
         const cudaError_t e = L->OT == 1   ? launch_narrow<XT, 1>(L, pl, X, Y, rows, im, st)
@@ -226,7 +236,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
     }
     float2* recW = nullptr;
     int* recO = nullptr;
-    if (pl.mode == kModeStaged) {
+    if (pl.mode == kModeStaged && !link.preW) {
         // K1: cell records, stream-ordered scratch (pool memory is retained, see alloc_layer)
         const size_t wbytes = static_cast<size_t>(L->pairs) * pl.rows_pad * sizeof(float2);
         const size_t obytes = static_cast<size_t>(L->pairs) * pl.row_tiles * pl.sh.OBLK * sizeof(int);
@@ -251,10 +261,12 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
     }
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
+    const float2* useW = link.preW ? link.preW : recW;
+    const int* useO = link.preW ? link.preO : recO;
     switch (L->OT) {
-        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
-        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
-        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, recW, recO, im, st); break;
+        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
+        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
+        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
     }
     if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
@@ -476,7 +488,101 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
 
 }  // namespace
 
+namespace {
+// Can layer A's gather epilogue produce layer B's cell records (fused chain)?
+// Both full (unsliced) layers, A not narrow, B staged, and neither forward
+// needs row chunking at this batch size.
+bool chain_fusable(const lmkan_b200_layer* A, const Plan& pa, const lmkan_b200_layer* B, int64_t rows, int cap,
+                   Plan& pb) {
+    if (A->n_out != A->n_out_total || B->n_out != B->n_out_total || A->n_out != B->n_in) return false;
+    if (pa.mode == kModeNarrow || A->device != B->device) return false;
+    if (!make_plan(B, rows, cap, pb) || pb.mode != kModeStaged) return false;
+    const lmkan_b200_layer* ls[2] = {A, B};
+    const Plan* ps[2] = {&pa, &pb};
+    for (int i = 0; i < 2; ++i) {
+        if (ps[i]->mode != kModeStaged) continue;
+        const size_t per_row = static_cast<size_t>(ls[i]->pairs) * (sizeof(float2) + sizeof(int) * 2);
+        if (static_cast<size_t>(rows) * per_row > record_scratch_cap()) return false;
+    }
+    return true;
+}
+}  // namespace
+
 namespace lmkan_b200::api {
+// model_infer of a fused model (model.hpp:268-315) on one stream: layer b's
+// gather epilogue writes layer b+1's cell records whenever chain_fusable, so
+// that activation never goes to memory and layer b+1 skips its K1; otherwise
+// the activation goes through acts[b & 1] as a plain forward.
+int forward_chain_f32(const lmkan_b200_layer* const* layers, int n, const float* X, float* Y, int64_t rows,
+                      void* const* acts, cudaStream_t st) {
+    if (rows == 0) return LMKAN_B200_OK;
+    const int cap = max_smem_optin(layers[0]->device);
+    ChainLink pending;
+    float2* pendW = nullptr;
+    int* pendO = nullptr;
+    const float* cur = X;
+    int rc = LMKAN_B200_OK;
+    for (int b = 0; b < n && rc == LMKAN_B200_OK; ++b) {
+        const lmkan_b200_layer* L = layers[b];
+        DeviceGuard g(L->device);
+        Plan pl;
+        if (!make_plan(L, rows, cap, pl))
+            return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
+        const bool last = b + 1 == n;
+        Plan pn;
+        const bool fuse = !last && (!pending.preW || pl.mode == kModeStaged) &&
+                          chain_fusable(L, pl, layers[b + 1], rows, cap, pn) &&
+                          env_int("LMKAN_B200_CHAIN_FUSE", 0) != 0;  // opt-in: measured slower
+        // a layer fed records by its predecessor must run its staged K2 on them
+        if (pending.preW && pl.mode != kModeStaged)
+            return fail(LMKAN_B200_EINVAL, "forward_chain: internal plan mismatch");
+        float* dst = last ? Y : static_cast<float*>(acts[b & 1]);
+        OutDests<float> out = single_dest<float>(dst, L->n_out);
+        ChainLink link = pending;
+        float2* emW = nullptr;
+        int* emO = nullptr;
+        if (fuse) {
+            const lmkan_b200_layer* N = layers[b + 1];
+            const size_t wbytes = static_cast<size_t>(N->pairs) * pn.rows_pad * sizeof(float2);
+            const size_t obytes = static_cast<size_t>(N->pairs) * pn.row_tiles * pn.sh.OBLK * sizeof(int);
+            cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&emW), wbytes, st);
+            if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&emO), obytes, st);
+            // rows in [rows, rows_pad) carry zero records (as K1 writes them); the last
+            // row tile's offset block is zeroed whole, the epilogue fills its valid rows
+            if (e == cudaSuccess && pn.rows_pad > rows)
+                e = cudaMemset2DAsync(emW + rows, pn.rows_pad * sizeof(float2), 0,
+                                      (pn.rows_pad - rows) * sizeof(float2), N->pairs, st);
+            if (e == cudaSuccess)
+                e = cudaMemset2DAsync(emO + (pn.row_tiles - 1) * pn.sh.OBLK, pn.row_tiles * pn.sh.OBLK * sizeof(int), 0,
+                                      pn.sh.OBLK * sizeof(int), N->pairs, st);
+            if (e != cudaSuccess) {
+                rc = cuda_fail(e, "forward_chain: record buffers");
+                break;
+            }
+            link.emit = EmitRecords{emW, emO, pn.sh, pn.rows_pad, pn.row_tiles, (N->G + pn.S - 1) / pn.S};
+            pl.smem = std::max<uint32_t>(pl.smem, emit_smem_bytes(pl.OT, pl.sh.R));  // staging for the record stores
+            link.gc_next = &N->gc;
+            out.n = 0;  // the activation lives on only as the next layer's records
+        }
+        rc = forward_rows<float>(L, pl, cur, out, rows, InputMap{}, st, nullptr, nullptr, link);
+        if (pendW) cudaFreeAsync(pendW, st);
+        if (pendO) cudaFreeAsync(pendO, st);
+        pendW = emW;
+        pendO = emO;
+        pending = ChainLink{};
+        if (fuse) {
+            pending.preW = emW;
+            pending.preO = emO;
+            cur = nullptr;  // a staged K2 reads only its records
+        } else {
+            cur = dst;
+        }
+    }
+    if (pendW) cudaFreeAsync(pendW, st);
+    if (pendO) cudaFreeAsync(pendO, st);
+    return rc;
+}
+
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 int cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
 int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,

@@ -476,6 +476,8 @@ int ensure_acts(lmkan_b200_model* M, int64_t rows, size_t elem, cudaStream_t st,
 
 template <typename XT>
 int run_chain(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStream_t st, void* const* acts) {
+    if constexpr (sizeof(XT) == 4)  // fp32: fused chain (next layer's records from the epilogue)
+        return api::forward_chain_f32(M->layers.data(), static_cast<int>(M->layers.size()), X, Y, rows, acts, st);
     const XT* cur = X;
     const size_t n = M->layers.size();
     for (size_t b = 0; b < n; ++b) {

@@ -180,3 +180,31 @@ def test_model_width_mismatch(pkg):
     model = pkg.Model.from_layers([a, b])
     with pytest.raises(ValueError, match="precond_forward: expected width 10, got 8"):
         model.infer(torch.randn((4, 6), device="cuda"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows", [777, 5000, 66000])
+def test_fused_chain_records_bitwise(pkg, monkeypatch, rows):
+    """Fused chain (each layer's epilogue writes the next layer's cell records,
+    skipping that layer's K1 and its activation round trip): bitwise equal to
+    the unfused chain and to the layers run one by one, for consecutive fusions
+    and ragged row counts."""
+    import torch
+    dims = [(16, 64, 8), (64, 96, 12), (96, 64, 8), (64, 2, 8)]
+    layers = [pkg.Layer.random(a, b, G, seed=20 + i) for i, (a, b, G) in enumerate(dims)]
+    X = torch.randn((rows, 16), device="cuda")
+    ref = X
+    for lay in layers:
+        ref = lay.forward(ref)
+    st = torch.cuda.Stream()
+    outs = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("LMKAN_B200_CHAIN_FUSE", fuse)
+        monkeypatch.setenv("LMKAN_B200_GRAPH", "0")
+        model = pkg.Model.from_layers(layers)
+        Y = torch.full((rows, 2), float("nan"), device="cuda")
+        with torch.cuda.stream(st):
+            model.infer_into(X, Y, st)
+        st.synchronize()
+        outs.append(Y)
+    assert torch.equal(outs[0], ref) and torch.equal(outs[1], ref)
