@@ -152,6 +152,11 @@ __device__ __forceinline__ float2 lds64_if(const void* p, bool pred) {
         : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_addr(p)), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -724,13 +729,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if constexpr (kSmemSheet) {
             if (lane == 0) {
                 const int slot = u % nbuf;
-                __threadfence_block();
-                if (atomicAdd(&cnt[slot], 1u) == NW - 1) {  // last warp out refills the slot
+                // acq_rel increment: releases this warp's reads of the slot (ordered
+                // before it by __syncwarp) and, for the last warp, acquires everyone
+                // else's, so all reads happen before the async-proxy overwrite below
+                if (atom_add_acq_rel_cta(&cnt[slot], 1u) == NW - 1) {  // last warp out refills the slot
                     cnt[slot] = 0;
                     if (u + nbuf < units) {
-                        // acquire side of the counter: every warp's reads of the slot (fenced
-                        // before its increment) happen before the async-proxy overwrite
-                        __threadfence_block();
                         fence_proxy_async();
                         issue(u + nbuf);
                     }
