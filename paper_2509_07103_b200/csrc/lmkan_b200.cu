@@ -90,8 +90,6 @@ constexpr int kRTChoices[] = {16, 8, 4};
 constexpr int kNumSMs = 148;
 constexpr int kMaxSlabs = 4;
 
-int rows_per_cta(int OT, int RT) { return shape_rt(OT, RT).R; }
-
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;

@@ -128,3 +128,16 @@ def test_backward_argument_errors(torch, pkg):
     sl = pkg.Layer.from_device(4, 3, 4, Pd.float(), 1.0, out_range=(0, 2))
     with pytest.raises(ValueError, match="output-sliced"):
         sl.backward(Pd, Xd, dYd[:, :2].contiguous())
+
+
+def test_backward_nonfinite_inputs_bitwise(torch, pkg, oracle):
+    """NaN / +-inf / huge inputs: the same bit patterns as the reference
+    (NaN propagation included), compared as raw 64-bit words."""
+    P, X, dY = _case(8, 6, 12, 40, seed=99)
+    X[0, 0], X[1, 1], X[2, 2], X[3, 3] = np.nan, np.inf, -np.inf, 1e300
+    X[4, :] = np.nan
+    layer = pkg.Layer.from_host(8, 6, 12, P, 0.8)
+    ref_dP, ref_dX = oracle.backward(12, P, X, dY, 0.8, workers=1)
+    got_dP, got_dX = layer.backward(P, X, dY, workers=1)
+    assert np.array_equal(got_dP.view(np.uint64), ref_dP.view(np.uint64))
+    assert np.array_equal(got_dX.view(np.uint64), ref_dX.view(np.uint64))
