@@ -67,6 +67,27 @@ def smem_ceiling(fma_per_row: float, sm_mhz, kernel_ms: float, rows: int) -> dic
             "frac": achieved / ceil_rows, "sm_mhz": mhz}
 
 
+def roofline_levels(achieved_gbs: float, fma_per_s: float, hbm_gbs: float, sm_mhz) -> dict:
+    """B_alg-based GB/s against HBM (MEASURED_PEAKS.json), L2 (tools/ubench_l2.cu,
+    profiles/r1_ubench_l2.json), the shared-memory port (148 x 128 B/clk) and
+    FMA/s against the FP32 pipe (148 x 128 FMA/clk), at the measured SM clock."""
+    mhz = float(sm_mhz or 1965.0)
+    l2 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ubench_l2.json")) as f:
+            l2 = float(json.load(f)["l2_read_gbs"])
+    except Exception:
+        pass
+    smem = 148 * 128 * mhz * 1e6 / 1e9
+    fp32 = 148 * 128 * mhz * 1e6
+    out = {"hbm": {"peak_gbs": hbm_gbs, "frac": achieved_gbs / hbm_gbs},
+           "smem": {"peak_gbs": smem, "frac": achieved_gbs / smem},
+           "fp32_fma": {"peak_fma_per_s": fp32, "frac": fma_per_s / fp32}}
+    if l2:
+        out["l2"] = {"peak_gbs": l2, "frac": achieved_gbs / l2, "source": "profiles/r1_ubench_l2.json"}
+    return out
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -485,7 +506,10 @@ def main():
                      "fp32_fma_tflops": fmas / (kernel_ms / 1e3) / 1e12,
                      # the ceiling that binds the gather: one 4-byte
                      # coefficient per FMA through the 128 B/clk/SM shared-memory port
-                     "smem_gather_ceiling": smem_ceiling(fmas / B, clocks.get("sm_mhz"), kernel_ms, B)},
+                     "smem_gather_ceiling": smem_ceiling(fmas / B, clocks.get("sm_mhz"), kernel_ms, B),
+                     # the same numerator against every level: > 1 means the
+                     # level is not binding (reuse above it); the SMEM frac is the binding one
+                     "levels": roofline_levels(achieved, fmas / (kernel_ms / 1e3), peak, clocks.get("sm_mhz"))},
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
