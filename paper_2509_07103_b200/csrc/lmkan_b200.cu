@@ -125,6 +125,8 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
 // Within a mode: prefer double buffering with the fewest slabs, then the
 // largest row tile that still fills the GPU with one wave of CTAs.
 bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
+    // ring depth: up to 4 (deeper rings measured no faster at cfg1-4; LMKAN_B200_MAX_NBUF overrides)
+    const int max_nbuf = std::max(2, std::min(16, env_int("LMKAN_B200_MAX_NBUF", 4)));
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
               force_s = env_int("LMKAN_B200_SLABS", 0);
     if (L->narrow) {
@@ -172,7 +174,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                     const ShapeRT sh = shape_rt(L->OT, RT, NW);
                     const int64_t tiles = (rows + sh.R - 1) / sh.R;
                     if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
-                    for (int nbuf = smem_sheet ? 4 : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
+                    for (int nbuf = smem_sheet ? max_nbuf : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
@@ -448,8 +450,11 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
+    // 8 chunks measured best at cfg2 (e2e 19.5 ms vs 20.7 / 22.4 / 23.8 for 4 / 12 / 16;
+    // a tapered first/last chunk measured 20.2): LMKAN_B200_HOST_CHUNKS overrides
     const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * 148 / std::max(1, L->n_ot);
-    int64_t chunk = std::max<int64_t>({(rows + 7) / 8, min_chunk, 1});
+    const int64_t nchunks = std::max(1, env_int("LMKAN_B200_HOST_CHUNKS", 8));
+    int64_t chunk = std::max<int64_t>({(rows + nchunks - 1) / nchunks, min_chunk, 1});
     chunk = std::min(chunk, rows);
     const size_t xb = static_cast<size_t>(chunk) * L->n_in * sizeof(XT);
     const size_t yb = static_cast<size_t>(chunk) * L->n_out * sizeof(XT);
