@@ -1,0 +1,566 @@
+// Gather-accumulate (stage 2: layer.hpp:116-133): K1 records_kernel and the
+// K2 / K3 fwd_fused_kernel with its plan shapes and shared-memory layout.
+#pragma once
+
+#include "locate.cuh"
+
+namespace lmkan_b200 {
+
+// Kernel variants of the layer forward.
+enum : int {
+    kModeFused = 0,   // K3: cells located in-kernel (warp-local), sheets via bulk copy
+    kModeStaged = 1,  // K2: cell records produced by K1 (records_kernel), sheets + records via bulk copy
+    kModeGlobal = 2,  // fallback for sheets larger than shared memory: in-kernel locate, sheets read from L2
+    kModeNarrow = 3,  // K4: n_out <= 4, whole table resident in shared memory, lanes over pairs
+};
+
+// Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
+template <int OT, int RT, int NW = kWarps>
+struct FusedShape {
+    static constexpr int LPR = OT / 4;               // lanes covering one row's OT outputs (float4 each)
+    static constexpr int RPW = 32 / LPR;             // rows per warp per gather instruction
+    static constexpr int ROWS_W = RPW * RT;          // rows owned by one warp
+    static constexpr int LOC = (ROWS_W + 31) / 32;   // cells each lane locates per pair (fused mode)
+    static constexpr int R = NW * ROWS_W;             // rows per CTA
+    static constexpr int OSTRIDE = RT + (RPW > 2 ? 4 : 0);  // padded per-lane-group offset run (bank spread)
+    static constexpr int OBLK = NW * RPW * OSTRIDE;         // offset ints per CTA per pair
+};
+// Runtime twin of FusedShape for host code / K1.
+struct ShapeRT {
+    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK, NW;
+    int lgRPW, lgROWS_W, lgR;  // RPW, ROWS_W, R are powers of two (OT, RT, NW are)
+};
+__host__ __device__ constexpr int ilog2(int v) { return v > 1 ? 1 + ilog2(v >> 1) : 0; }
+__host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps) {
+    ShapeRT s;
+    s.OT = OT;
+    s.RT = RT;
+    s.NW = NW;
+    s.LPR = OT / 4;
+    s.RPW = 32 / s.LPR;
+    s.ROWS_W = s.RPW * RT;
+    s.R = NW * s.ROWS_W;
+    s.OSTRIDE = RT + (s.RPW > 2 ? 4 : 0);
+    s.OBLK = NW * s.RPW * s.OSTRIDE;
+    s.lgRPW = ilog2(s.RPW);
+    s.lgROWS_W = ilog2(s.ROWS_W);
+    s.lgR = ilog2(s.R);
+    return s;
+}
+// Position of CTA-local row qc's node offset inside the CTA's offset block: the
+// RT rows a lane group gathers are contiguous, so a thread loads them as int4s.
+__host__ __device__ inline int offset_slot(const ShapeRT& s, int qc) {
+    const int warp = qc >> s.lgROWS_W, q = qc & (s.ROWS_W - 1);
+    const int sub = q & (s.RPW - 1), j = q >> s.lgRPW;
+    return (warp * s.RPW + sub) * s.OSTRIDE + j;
+}
+
+// Fused chain (model_infer of a fused model, model.hpp:268-315): the NEXT
+// layer's cell records written by this layer's epilogue. Its 4 consecutive
+// outputs per lane are two input pairs of the next layer, located right there
+// (next layer's grid, gc_next) and stored in the next layer's K2 order, so
+// the activation never round-trips through HBM and the next K1 is skipped.
+// Shared memory the emitting epilogue needs (one pass: OT/4 pairs x R rows).
+// + the next layer's grid constants (thresholds, points, inverse widths), so the
+// locates read shared memory instead of divergent parameter-space loads.
+__host__ __device__ inline uint32_t emit_smem_bytes(int OT, int R) {
+    return static_cast<uint32_t>(OT / 4) * R * 12u + kMaxThr * 4u + (kMaxThr + 1) * 8u + kMaxThr * 8u + 16u;
+}
+struct EmitRecords {
+    float2* W;  // [pairs'][rows_pad'] {alpha, gamma}; nullptr: no emission
+    int* O;     // [pairs'][tiles'][OBLK'] packed offsets
+    ShapeRT sh;  // next layer's K2 row shape
+    int64_t rows_pad, tiles;
+    int H;  // next layer's slab height
+};
+
+// Record-ring depth of the staged mode: records of pair p arrive with its first
+// slab and must outlive its S slabs while up to NBUF units are in flight.
+__host__ __device__ inline int staged_nrec(int nbuf, int S) { return (nbuf - 1 + S - 1) / S + 1; }
+
+// Shared-memory carve-up (host and device agree on it).
+//   sheets : NBUF x slab buffers of (H+1)(G+1) x OT fp32 (bulk-copy destinations)
+//   records: NREC x {R float2 {alpha, gamma}, OBLK packed offsets}; NREC = staged_nrec
+//            when staged (they arrive with a pair's first slab), else 1
+//            (warp-private, written by the in-kernel locate)
+//   grid constants (not staged): thresholds, points[G+1], inv_h[G] (fp64)
+//   NBUF "landed" mbarriers + NBUF finished-warp counters
+struct FusedSmem {
+    uint32_t sheet_bytes, recw_bytes, reco_bytes, off_recw, off_reco, off_thr, off_pts, off_inv, off_bar,
+        off_cnt, total;
+    int nrec;
+};
+__host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1,
+                                                       int NW = kWarps) {
+    const ShapeRT sh = shape_rt(OT, RT, NW);
+    const int H = (G + S - 1) / S;
+    const int nb = nbuf > 0 ? nbuf : 1;
+    FusedSmem s;
+    s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
+    s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * OT * 4u;
+    s.recw_bytes = sh.R * 8u;  // float2 {alpha, gamma} per row
+    s.reco_bytes = sh.OBLK * 4u;
+    uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
+    o = (o + 127u) & ~127u;
+    s.off_recw = o;
+    o += s.nrec * s.recw_bytes;
+    s.off_reco = o;
+    o += s.nrec * s.reco_bytes;
+    o = (o + 15u) & ~15u;
+    s.off_thr = o;
+    s.off_pts = o;
+    s.off_inv = o;
+    if (mode != kModeStaged) {
+        o += kMaxThr * 8u;
+        s.off_pts = o;
+        o += (kMaxThr + 1) * 8u;
+        o = (o + 15u) & ~15u;
+        s.off_inv = o;
+        o += static_cast<uint32_t>(G) * 8u;  // inv_h
+        o = (o + 15u) & ~15u;
+    }
+    s.off_bar = o;
+    o += 8u * nb;
+    s.off_cnt = o;
+    o += 4u * nb;
+    s.total = (o + 127u) & ~127u;
+    return s;
+}
+
+// K1 (staged path): cell records for every (pair, row) in the order K2 consumes
+// them. A CTA stages a 64-row x 16-pair X tile through shared memory (row-
+// contiguous loads), locates each (row, pair) and writes
+//   W[p][row]                        = {alpha, gamma}            (coalesced)
+//   O[p][tile][offset_slot(row % R)] = packed slab / node offset
+// Rows in [rows, rows_pad) get zero records (their outputs are discarded).
+template <typename XT>
+__global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
+                                                      int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
+                                                      int H, float2* __restrict__ W, int* __restrict__ O,
+                                                      const InputMap im) {
+    __shared__ XT xs[64][33];
+    __shared__ int64_t rbase[64];
+    __shared__ int coff[32];
+    __shared__ XT thr[kMaxThr];
+    __shared__ double pts[kMaxThr + 1];
+    __shared__ double invh[kMaxThr];
+    const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
+    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
+    for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
+    const int p0 = blockIdx.y * 16;
+    const int r = tid & 63, pq = tid >> 6;
+    const int64_t tiles = rows_pad >> sh.lgR;
+    // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
+    // (thresholds, points, inverse widths) is amortized over many tiles
+    for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64; r0 < rows_pad; r0 += static_cast<int64_t>(gridDim.x) * 64) {
+        __syncthreads();  // previous tile's xs / rbase fully consumed
+        if (tid < 64) rbase[tid] = in_rowbase(im, r0 + tid, n_in);
+        if (tid < 32) coff[tid] = in_coloff(im, 2 * p0 + tid);
+        __syncthreads();
+        XT v[8];  // all 8 loads of this thread in flight before any store
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int i = tid + 256 * t;
+            const int rr = i >> 5, c = i & 31;
+            const int col = 2 * p0 + c;
+            v[t] = (r0 + rr < rows && col < n_in) ? __ldg(X + rbase[rr] + coff[c]) : XT(0);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int i = tid + 256 * t;
+            xs[i >> 5][i & 31] = v[t];
+        }
+        __syncthreads();
+        // thread = (row r of the tile, pairs pq, pq+4, pq+8, pq+12 of the block):
+        // the row's tile / offset slot are computed once, record addresses step
+        // by whole pairs
+        const int64_t g = r0 + r;
+        if (g < rows_pad) {  // row tiles (R) may be shorter than the 64-row X tile
+            const int64_t tile = g >> sh.lgR;
+            const int slot = offset_slot(sh, static_cast<int>(g & (sh.R - 1)));
+            float2* wp = W + static_cast<size_t>(p0 + pq) * rows_pad + g;
+            int* op = O + (static_cast<size_t>(p0 + pq) * tiles + tile) * sh.OBLK + slot;
+            const size_t wstep = static_cast<size_t>(4) * rows_pad, ostep = static_cast<size_t>(4) * tiles * sh.OBLK;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int pl = pq + 4 * k;
+                if (p0 + pl < pairs) {
+                    float2 ag = make_float2(0.f, 0.f);
+                    int packed = 0;
+                    if (g < rows)
+                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.OT, H, ag);
+                    *wp = ag;
+                    *op = packed;
+                }
+                wp += wstep;
+                op += ostep;
+            }
+        }
+    }
+}
+
+// K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
+// Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
+// [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of
+// it — is one contiguous bulk copy, and each node's OT outputs are a
+// contiguous, float4-aligned run.
+//
+// Pipeline over units u = (pair p, slab s), no CTA-wide barrier in the loop:
+//   * sheets (+ the pair's records when staged): NBUF-deep ring in shared memory
+//     filled by the bulk-copy engine; "full[slot]" mbarriers count landed bytes.
+//     The LAST warp to finish with a slot (shared-memory atomic counter) issues
+//     the copy that refills it, so no warp waits on a producer and none is
+//     dedicated to producing.
+//   * fused mode: every warp locates the cells of its own rows for the next pair
+//     into a warp-private record slice (x pair prefetched a pair ahead).
+//   * gather: lane group `sub` handles one row, lane c4 a float4 of outputs; per
+//     row one LDS.64 of {alpha, gamma} (one wavefront for the warp's rows; an
+//     LDS.128 of four weights would cost two) and 4 LDS.128 of coefficients
+//     (nodes n, n+1, n+G+1, n+G+2), 16 FMAs; a lane group's RT node offsets are contiguous
+//     (int4 loads, kept in registers across the pair's slabs). With slabs
+//     (SLAB = true) a row is gathered only during its cell's slab.
+//
+// Accumulation order per (row, output): acc = 0; for p: acc += t_p with
+// t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
+// reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
+// Deterministic: no data atomics, fixed order, independent of the launch shape.
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
+                     const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
+                     const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
+                     const int* __restrict__ recO, int64_t rows_pad, const InputMap im, const EmitRecords emit,
+                     const __grid_constant__ GridConst gc_next) {
+    using Sh = FusedShape<OT, RT, NW>;
+    constexpr int R = Sh::R;
+    constexpr int NT = NW * 32;
+    constexpr bool kSmemSheet = MODE != kModeGlobal;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int G = gc.G;
+    const int nodes = (G + 1) * (G + 1);
+    const int H = (G + S - 1) / S;
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW);
+    float* sheets = reinterpret_cast<float*>(smem);
+    float2* rec_w = reinterpret_cast<float2*>(smem + L.off_recw);
+    int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
+    XT* thr = reinterpret_cast<XT*>(smem + L.off_thr);
+    double* pts = reinterpret_cast<double*>(smem + L.off_pts);
+    double* inv = reinterpret_cast<double*>(smem + L.off_inv);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+    unsigned* cnt = reinterpret_cast<unsigned*>(smem + L.off_cnt);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int sub = lane / Sh::LPR, c4 = lane % Sh::LPR;
+    const int64_t tile = blockIdx.x;
+    const int64_t row0 = tile * R;
+    const int ot = blockIdx.y;
+    const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
+    const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * OT;
+    const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * OT;  // slab stride within a sheet
+    const int64_t tiles = rows_pad / R;
+    const int units = pairs * S;
+
+    if constexpr (MODE != kModeStaged) {
+        for (int k = tid; k < kMaxThr; k += NT) thr[k] = thr_of<XT>(gc)[k];
+        for (int k = tid; k <= G; k += NT) pts[k] = gc.points[k];
+        for (int k = tid; k < G; k += NT) inv[k] = gc.inv_h[k];
+    }
+    uint64_t policy = 0, policy_rec = 0;
+    if constexpr (kSmemSheet) {
+        if (tid == 0) {
+            for (int s = 0; s < nbuf; ++s) {
+                mbar_init(&full[s], 1);
+                cnt[s] = 0;
+            }
+            fence_barrier_init();
+        }
+        policy = policy_evict_last();
+        policy_rec = policy_evict_first();
+    }
+    __syncthreads();
+
+    auto issue = [&](int u) {  // one thread: slab (+ the pair's records when staged) of unit u
+        const int p = u / S, s = u - p * S;
+        const int slot = u % nbuf;
+        const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * OT * 4u;
+        const bool with_rec = MODE == kModeStaged && s == 0;
+        mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? L.recw_bytes + L.reco_bytes : 0u));
+        const char* src =
+            reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * sheet_floats + static_cast<size_t>(s) * slab_floats);
+        char* dst = reinterpret_cast<char*>(sheets) + static_cast<size_t>(slot) * L.sheet_bytes;
+        constexpr uint32_t kChunk = 32768;
+        for (uint32_t o = 0; o < bytes; o += kChunk) {
+            const uint32_t n = bytes - o < kChunk ? bytes - o : kChunk;
+            bulk_g2s(dst + o, src + o, n, &full[slot], policy);
+        }
+        if constexpr (MODE == kModeStaged) {
+            if (with_rec) {
+                const int rs = p % L.nrec;
+                bulk_g2s(reinterpret_cast<char*>(rec_w) + rs * L.recw_bytes,
+                         recW + static_cast<size_t>(p) * rows_pad + row0, L.recw_bytes, &full[slot], policy_rec);
+                bulk_g2s(reinterpret_cast<char*>(rec_o) + rs * L.reco_bytes,
+                         recO + (static_cast<size_t>(p) * tiles + tile) * Sh::OBLK, L.reco_bytes, &full[slot],
+                         policy_rec);
+            }
+        }
+    };
+    if constexpr (kSmemSheet) {
+        if (tid == 0) {
+            const int pre = nbuf < units ? nbuf : units;
+            for (int u = 0; u < pre; ++u) issue(u);
+        }
+    }
+
+    // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane
+    XT xa[Sh::LOC], xb[Sh::LOC];
+    const XT* xrow[Sh::LOC];
+    // float2 x-pair loads when both columns are adjacent and 8-byte aligned
+    const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0 && (!im.conv || (im.C & 1) == 0);
+#pragma unroll
+    for (int k = 0; k < Sh::LOC; ++k) {
+        const int q = k * 32 + lane;
+        const int64_t r = row0 + warp * Sh::ROWS_W + q;
+        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && r < rows) ? X + in_rowbase(im, r, n_in) : nullptr;
+    }
+    auto prefetch = [&](int p) {
+        const int c0 = in_coloff(im, 2 * p), c1 = im.conv ? in_coloff(im, 2 * p + 1) : c0 + 1;
+#pragma unroll
+        for (int k = 0; k < Sh::LOC; ++k) {
+            if (xrow[k]) {
+                if (sizeof(XT) == 4 && x_vec_ok) {
+                    const float2 v = __ldg(reinterpret_cast<const float2*>(xrow[k] + c0));
+                    xa[k] = v.x;
+                    xb[k] = v.y;
+                } else {
+                    xa[k] = __ldg(xrow[k] + c0);
+                    xb[k] = __ldg(xrow[k] + c1);
+                }
+            } else {
+                xa[k] = xb[k] = XT(0);
+            }
+        }
+    };
+    auto locate = [&]() {
+        const ShapeRT shp = shape_rt(OT, RT, NW);
+#pragma unroll
+        for (int k = 0; k < Sh::LOC; ++k) {
+            const int q = k * 32 + lane;
+            if (q < Sh::ROWS_W) {
+                float2 ag = make_float2(0.f, 0.f);
+                int packed = 0;
+                if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, OT, H, ag);
+                const int qc = warp * Sh::ROWS_W + q;
+                rec_w[qc] = ag;
+                rec_o[offset_slot(shp, qc)] = packed;
+            }
+        }
+    };
+
+    float4 acc[RT];
+#pragma unroll
+    for (int j = 0; j < RT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int rstride = (G + 1) * OT;  // node (i1+1, i2) is (G+1) nodes further
+
+    if constexpr (MODE != kModeStaged) {
+        prefetch(0);
+        locate();
+        if (pairs > 1) prefetch(1);
+        __syncwarp();
+    }
+    int offs[RT];
+    const float2* rw = rec_w;
+    int p = 0, s = 0;
+    for (int u = 0; u < units; ++u) {
+        const float* sh;
+        if constexpr (kSmemSheet) {
+            const int slot = u % nbuf;
+            mbar_wait(&full[slot], static_cast<uint32_t>((u / nbuf) & 1));
+            sh = sheets + static_cast<size_t>(slot) * (L.sheet_bytes / 4) + 4 * c4;
+        } else {
+            sh = tsrc + static_cast<size_t>(p) * sheet_floats + 4 * c4;
+        }
+        if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets to registers (kept across slabs)
+            const int rs = MODE == kModeStaged ? p % L.nrec : 0;
+            rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
+            const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
+#pragma unroll
+            for (int k = 0; k < RT / 4; ++k) {
+                const int4 v = reinterpret_cast<const int4*>(ro)[k];
+                offs[4 * k] = v.x;
+                offs[4 * k + 1] = v.y;
+                offs[4 * k + 2] = v.z;
+                offs[4 * k + 3] = v.w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < RT; ++j) {
+            float4 w, p00, p01, p10, p11;
+            if constexpr (SLAB) {
+                // rows whose cell lies in another slab load nothing and add +0
+                const bool v = (offs[j] >> kSlabShift) == s;
+                const float* b0 = sh + (offs[j] & kOffMask);
+                const float* b1 = b0 + rstride;
+                w = weights_ag(lds64_if(rw + j * Sh::RPW, v));
+                p00 = lds128_if(b0, v);
+                p01 = lds128_if(b0 + OT, v);
+                p10 = lds128_if(b1, v);
+                p11 = lds128_if(b1 + OT, v);
+            } else {
+                w = weights_ag(rw[j * Sh::RPW]);
+                const float* b0 = sh + offs[j];
+                const float* b1 = b0 + rstride;
+                if constexpr (kSmemSheet) {
+                    p00 = *reinterpret_cast<const float4*>(b0);
+                    p01 = *reinterpret_cast<const float4*>(b0 + OT);
+                    p10 = *reinterpret_cast<const float4*>(b1);
+                    p11 = *reinterpret_cast<const float4*>(b1 + OT);
+                } else {
+                    p00 = __ldg(reinterpret_cast<const float4*>(b0));
+                    p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
+                    p10 = __ldg(reinterpret_cast<const float4*>(b1));
+                    p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+                }
+            }
+            acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
+            acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
+            acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
+            acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
+        }
+        __syncwarp();  // this warp is done with slot u % nbuf (and, at s == S-1, with pair p's records)
+        if constexpr (kSmemSheet) {
+            if (lane == 0) {
+                const int slot = u % nbuf;
+                // acq_rel increment: releases this warp's reads of the slot (ordered
+                // before it by __syncwarp) and, for the last warp, acquires everyone
+                // else's, so all reads happen before the async-proxy overwrite below
+                if (atom_add_acq_rel_cta(&cnt[slot], 1u) == NW - 1) {  // last warp out refills the slot
+                    cnt[slot] = 0;
+                    if (u + nbuf < units) {
+                        fence_proxy_async();
+                        issue(u + nbuf);
+                    }
+                }
+            }
+        }
+        if (++s == S) {
+            s = 0;
+            ++p;
+            if constexpr (MODE != kModeStaged) {
+                if (p < pairs) {
+                    locate();
+                    if (p + 1 < pairs) prefetch(p + 1);
+                    __syncwarp();
+                }
+            }
+        }
+    }
+
+    // epilogue: y *= gamma (layer.hpp:131), masked store of the warp's rows into
+    // every destination (peer destinations are NVLink stores issued as the
+    // CTA's tile completes, overlapping the other CTAs' gathers)
+    const int col = ot * OT + 4 * c4;
+#pragma unroll
+    for (int j = 0; j < RT; ++j) acc[j] = make_float4(acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma,
+                                                      acc[j].w * gamma);
+    if constexpr (sizeof(XT) == 4) {
+        if (emit.W) {
+            // fused chain: this lane's outputs col..col+3 are the next layer's pairs
+            // col/2 and col/2 + 1. Two passes (h = 0, 1), one next-layer pair per lane
+            // each: locate into shared memory [pair][row], then coalesced record
+            // stores — rows run contiguously in W, and when both layers use the same
+            // row tile the CTA's offset block of each pair is written whole.
+            constexpr int PP = OT / 4;  // next-layer pairs per pass
+            float2* sW = reinterpret_cast<float2*>(smem);
+            int* sO = reinterpret_cast<int*>(smem + static_cast<size_t>(PP) * R * sizeof(float2));
+            unsigned char* gbase = smem + static_cast<size_t>(PP) * R * 12u;
+            double* npts = reinterpret_cast<double*>(gbase);
+            double* ninv = npts + kMaxThr + 1;
+            float* nthr = reinterpret_cast<float*>(ninv + kMaxThr);
+            const int pn_base = (ot * OT) >> 1;
+            const int pairs_next = n_out >> 1;
+            const bool same_tile = emit.sh.R == R;
+            __syncthreads();  // all warps past the gather loop: the ring space is free
+            for (int k = tid; k < kMaxThr + 1; k += NT) {
+                npts[k] = gc_next.points[k];
+                if (k < kMaxThr) {
+                    ninv[k] = gc_next.inv_h[k];
+                    nthr[k] = gc_next.t32[k];
+                }
+            }
+            for (int h = 0; h < 2; ++h) {
+                __syncthreads();  // grid constants in place / the previous pass's stores done
+#pragma unroll
+                for (int j = 0; j < RT; ++j) {
+                    const int rl = warp * Sh::ROWS_W + j * Sh::RPW + sub;
+                    const int64_t r = row0 + rl;
+                    float2 ag = make_float2(0.f, 0.f);
+                    int packed = 0;
+                    if (r < rows && col + 2 * h + 1 < n_out) {
+                        const float a = h ? acc[j].z : acc[j].x, b = h ? acc[j].w : acc[j].y;
+                        packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.OT, emit.H, ag);
+                    }
+                    sW[c4 * R + rl] = ag;
+                    sO[c4 * R + rl] = packed;
+                }
+                __syncthreads();
+                for (int idx = tid; idx < PP * R; idx += NT) {
+                    const int pl = idx / R, rl = idx - pl * R;
+                    const int pn = pn_base + 2 * pl + h;
+                    const int64_t r = row0 + rl;
+                    if (pn < pairs_next && r < emit.rows_pad) emit.W[static_cast<size_t>(pn) * emit.rows_pad + r] = sW[idx];
+                }
+                if (same_tile) {  // the whole offset block of (pair, tile), slot order, padding slots zeroed
+                    const int ob = emit.sh.OBLK;
+                    for (int idx = tid; idx < PP * ob; idx += NT) {
+                        const int pl = idx / ob, sl = idx - pl * ob;
+                        const int pn = pn_base + 2 * pl + h;
+                        if (pn >= pairs_next) continue;
+                        const int grp = sl / emit.sh.OSTRIDE, jj = sl - grp * emit.sh.OSTRIDE;
+                        int v = 0;
+                        if (jj < emit.sh.RT) {
+                            const int q = (grp / emit.sh.RPW) * emit.sh.ROWS_W + jj * emit.sh.RPW + grp % emit.sh.RPW;
+                            v = sO[pl * R + q];
+                        }
+                        emit.O[(static_cast<size_t>(pn) * emit.tiles + tile) * ob + sl] = v;
+                    }
+                } else {
+                    for (int idx = tid; idx < PP * R; idx += NT) {
+                        const int pl = idx / R, rl = idx - pl * R;
+                        const int pn = pn_base + 2 * pl + h;
+                        const int64_t r = row0 + rl;
+                        if (pn >= pairs_next || r >= emit.rows_pad) continue;
+                        const int slot = offset_slot(emit.sh, static_cast<int>(r & (emit.sh.R - 1)));
+                        emit.O[(static_cast<size_t>(pn) * emit.tiles + (r >> emit.sh.lgR)) * emit.sh.OBLK + slot] =
+                            sO[idx];
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxDest; ++d) {  // unrolled: constant indices keep `out` in the parameter space
+        if (d >= out.n) break;
+        XT* const base = out.base[d] + out.col0;
+        const bool y_vec_ok = (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (out.ld & 3) == 0;
+#pragma unroll
+        for (int j = 0; j < RT; ++j) {
+            const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
+            if (r >= rows) continue;
+            XT* yr = base + r * out.ld;
+            if constexpr (sizeof(XT) == 4) {
+                if (col + 3 < n_out && y_vec_ok) {
+                    *reinterpret_cast<float4*>(yr + col) = acc[j];
+                    continue;
+                }
+            }
+            const float v[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (col + e < n_out) yr[col + e] = static_cast<XT>(v[e]);
+        }
+    }
+}
+
+}  // namespace lmkan_b200
