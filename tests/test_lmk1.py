@@ -208,3 +208,38 @@ def test_fused_chain_records_bitwise(pkg, monkeypatch, rows):
         st.synchronize()
         outs.append(Y)
     assert torch.equal(outs[0], ref) and torch.equal(outs[1], ref)
+
+
+def _write_lmk1(path, blocks, dtype="f32"):
+    """Minimal LMK1 writer for pure-lookup models (serialize.hpp:109-183 format:
+    magic, u32 LE header length, JSON header, LE payload P[i1][i2][pair][out])."""
+    elem = 4 if dtype == "f32" else 8
+    hb = {"blocks": [], "dtype": dtype, "format": "LMK1", "tensors": [], "version": 1}
+    payload = []
+    for i, (n_in, n_out, G, P) in enumerate(blocks):
+        hb["blocks"].append({"G": G, "gamma": 1.0, "mode": "none", "n_in": n_in, "n_out": n_out, "type": "lmkan"})
+        hb["tensors"].append({"bytes": P.size * elem, "name": f"block{i}.P", "shape": list(P.shape)})
+        payload.append(np.ascontiguousarray(P, "<f4" if elem == 4 else "<f8").tobytes())
+    h = json.dumps(hb, separators=(",", ":")).encode()
+    with open(path, "wb") as f:
+        f.write(b"LMK1" + len(h).to_bytes(4, "little") + h + b"".join(payload))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_lmk1_multichunk_stream(pkg, tmp_path, dtype):
+    """A block larger than the 64 MB staging chunk (several double-buffered
+    chunks, chunk boundaries inside a node): the device table equals the
+    payload rounded to fp32, for the whole layer and for an output slice."""
+    rng = np.random.default_rng(3)
+    n_in, n_out, G = 512, 520, 16  # 289 * 256 * 520 values: 154 MB f32, 308 MB f64
+    P = rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)).astype(np.float32).astype(np.float64)
+    path = str(tmp_path / "big.lmk1")
+    _write_lmk1(path, [(n_in, n_out, G, P), (n_out, 4, 8, rng.standard_normal((9, 9, n_out // 2, 4)))], dtype)
+    assert pkg.lmk1_inspect(path)["blocks"] == 2
+    lay = pkg.Layer.load_lmk1(path, 0)
+    want = P.astype(np.float32).astype(np.float64)
+    for pb, pe in [(0, 40), (200, 256)]:
+        assert np.array_equal(lay.read_table(pb, pe), want[:, :, pb:pe, :])
+    sl = pkg.Layer.load_lmk1(path, 0, out_range=(100, 333))
+    assert np.array_equal(sl.read_table(10, 30), want[:, :, 10:30, 100:333])
