@@ -173,7 +173,10 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                     }
                     const ShapeRT sh = shape_rt(L->OT, RT, NW);
                     const int64_t tiles = (rows + sh.R - 1) / sh.R;
-                    if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot < kNumSMs) continue;
+                    // a taller row tile reuses each sheet for more rows; take it while the
+                    // grid still covers >= 3/4 of the SMs (cfg4: RT 16 with 128 CTAs 0.392 ms
+                    // beat RT 8 with 256 CTAs = 1.7 waves, 0.404 ms)
+                    if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot * 4 < kNumSMs * 3) continue;
                     for (int nbuf = smem_sheet ? max_nbuf : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
