@@ -185,7 +185,8 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, in
                           int32_t* i2, float* w, int64_t rows, void* stream);
 
 /* Tuning / introspection: kernel variant chosen for `rows` (OT = output tile,
- * RT = rows per thread, NBUF = sheet buffers, rows_per_cta), the number of
+ * RT = rows per thread, NBUF = sheet buffers, rows_per_cta = the row tile,
+ * possibly shortened so the grid fills whole waves of SMs), the number of
  * kernel launches one forward issues, the mode (0 = fused locate+gather,
  * 1 = staged: cell-record kernel + gather kernel, 2 = global-sheet fallback)
  * the number of i1-slabs a sheet is streamed in and the warps per CTA (16,

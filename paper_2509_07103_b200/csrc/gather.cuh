@@ -133,11 +133,11 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
 //   W[p][row]                        = {alpha, gamma}            (coalesced)
 //   O[p][tile][offset_slot(row % R)] = packed slab / node offset
 // Rows in [rows, rows_pad) get zero records (their outputs are discarded).
-template <typename XT>
+template <typename XT, bool SHORT_TILES>
 __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
                                                       int H, float2* __restrict__ W, int* __restrict__ O,
-                                                      const InputMap im) {
+                                                      const InputMap im, int64_t Rt) {
     __shared__ XT xs[64][33];
     __shared__ int64_t rbase[64];
     __shared__ int coff[32];
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
     const int p0 = blockIdx.y * 16;
     const int r = tid & 63, pq = tid >> 6;
-    const int64_t tiles = rows_pad >> sh.lgR;
+    const int64_t tiles = SHORT_TILES ? rows_pad / Rt : rows_pad >> sh.lgR;  // K2 row tiles of Rt <= R rows
     // row tiles of 64 are strided over gridDim.x, so the per-CTA setup above
     // (thresholds, points, inverse widths) is amortized over many tiles
     for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64; r0 < rows_pad; r0 += static_cast<int64_t>(gridDim.x) * 64) {
@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
         // by whole pairs
         const int64_t g = r0 + r;
         if (g < rows_pad) {  // row tiles (R) may be shorter than the 64-row X tile
-            const int64_t tile = g >> sh.lgR;
-            const int slot = offset_slot(sh, static_cast<int>(g & (sh.R - 1)));
+            const int64_t tile = SHORT_TILES ? g / Rt : g >> sh.lgR;  // shortened tiles: a real division
+            const int slot = offset_slot(sh, static_cast<int>(g - tile * Rt));
             float2* wp = W + static_cast<size_t>(p0 + pq) * rows_pad + g;
             int* op = O + (static_cast<size_t>(p0 + pq) * tiles + tile) * sh.OBLK + slot;
             const size_t wstep = static_cast<size_t>(4) * rows_pad, ostep = static_cast<size_t>(4) * tiles * sh.OBLK;
@@ -225,15 +225,16 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW, bool TAIL>
 __global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im, const EmitRecords emit,
-                     const __grid_constant__ GridConst gc_next) {
+                     const __grid_constant__ GridConst gc_next, int Rt_arg) {
     using Sh = FusedShape<OT, RT, NW>;
     constexpr int R = Sh::R;
+    const int Rt = TAIL ? Rt_arg : R;  // full-tile kernels keep the row tile a compile-time constant
     constexpr int NT = NW * 32;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -254,12 +255,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const int sub = lane / Sh::LPR, c4 = lane % Sh::LPR;
     const int64_t tile = blockIdx.x;
-    const int64_t row0 = tile * R;
+    // row tiles of Rt <= R rows (Rt < R balances the grid over the SMs): lane
+    // slots q >= Rt and rows >= rows are masked, issuing no gathers
+    const int64_t row0 = tile * Rt;
     const int ot = blockIdx.y;
     const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
     const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * OT;
     const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * OT;  // slab stride within a sheet
-    const int64_t tiles = rows_pad / R;
+    const int64_t tiles = rows_pad / Rt;
+    const uint32_t recw_copy = static_cast<uint32_t>(Rt) * 8u;  // this tile's records (<= L.recw_bytes)
     const int units = pairs * S;
 
     if constexpr (MODE != kModeStaged) {
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int slot = u % nbuf;
         const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * OT * 4u;
         const bool with_rec = MODE == kModeStaged && s == 0;
-        mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? L.recw_bytes + L.reco_bytes : 0u));
+        mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? recw_copy + L.reco_bytes : 0u));
         const char* src =
             reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * sheet_floats + static_cast<size_t>(s) * slab_floats);
         char* dst = reinterpret_cast<char*>(sheets) + static_cast<size_t>(slot) * L.sheet_bytes;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (with_rec) {
                 const int rs = p % L.nrec;
                 bulk_g2s(reinterpret_cast<char*>(rec_w) + rs * L.recw_bytes,
-                         recW + static_cast<size_t>(p) * rows_pad + row0, L.recw_bytes, &full[slot], policy_rec);
+                         recW + static_cast<size_t>(p) * rows_pad + row0, recw_copy, &full[slot], policy_rec);
                 bulk_g2s(reinterpret_cast<char*>(rec_o) + rs * L.reco_bytes,
                          recO + (static_cast<size_t>(p) * tiles + tile) * Sh::OBLK, L.reco_bytes, &full[slot],
                          policy_rec);
@@ -322,7 +326,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int k = 0; k < Sh::LOC; ++k) {
         const int q = k * 32 + lane;
         const int64_t r = row0 + warp * Sh::ROWS_W + q;
-        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && r < rows) ? X + in_rowbase(im, r, n_in) : nullptr;
+        const bool in_tile = warp * Sh::ROWS_W + q < Rt;
+        xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && in_tile && r < rows) ? X + in_rowbase(im, r, n_in) : nullptr;
     }
     auto prefetch = [&](int p) {
         const int c0 = in_coloff(im, 2 * p), c1 = im.conv ? in_coloff(im, 2 * p + 1) : c0 + 1;
@@ -362,6 +367,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
     for (int j = 0; j < RT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int rstride = (G + 1) * OT;  // node (i1+1, i2) is (G+1) nodes further
+    // The planner makes Rt a multiple of ROWS_W, so a warp's rows are all inside
+    // the tile or all beyond it: warps beyond it issue no gathers. Rows past the
+    // batch end inside the last tile gather zero-weight records (no branch in
+    // the hot loop) and are not stored.
+    const bool warp_live = warp * Sh::ROWS_W < Rt;
 
     if constexpr (MODE != kModeStaged) {
         prefetch(0);
@@ -394,39 +404,41 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 offs[4 * k + 3] = v.w;
             }
         }
+        if (!TAIL || warp_live) {  // TAIL: shortened row tiles, some warps hold no rows
 #pragma unroll
-        for (int j = 0; j < RT; ++j) {
-            float4 w, p00, p01, p10, p11;
-            if constexpr (SLAB) {
-                // rows whose cell lies in another slab load nothing and add +0
-                const bool v = (offs[j] >> kSlabShift) == s;
-                const float* b0 = sh + (offs[j] & kOffMask);
-                const float* b1 = b0 + rstride;
-                w = weights_ag(lds64_if(rw + j * Sh::RPW, v));
-                p00 = lds128_if(b0, v);
-                p01 = lds128_if(b0 + OT, v);
-                p10 = lds128_if(b1, v);
-                p11 = lds128_if(b1 + OT, v);
-            } else {
-                w = weights_ag(rw[j * Sh::RPW]);
-                const float* b0 = sh + offs[j];
-                const float* b1 = b0 + rstride;
-                if constexpr (kSmemSheet) {
-                    p00 = *reinterpret_cast<const float4*>(b0);
-                    p01 = *reinterpret_cast<const float4*>(b0 + OT);
-                    p10 = *reinterpret_cast<const float4*>(b1);
-                    p11 = *reinterpret_cast<const float4*>(b1 + OT);
+            for (int j = 0; j < RT; ++j) {
+                float4 w, p00, p01, p10, p11;
+                if constexpr (SLAB) {
+                    // rows whose cell lies in another slab load nothing and add +0
+                    const bool v = (offs[j] >> kSlabShift) == s;
+                    const float* b0 = sh + (offs[j] & kOffMask);
+                    const float* b1 = b0 + rstride;
+                    w = weights_ag(lds64_if(rw + j * Sh::RPW, v));
+                    p00 = lds128_if(b0, v);
+                    p01 = lds128_if(b0 + OT, v);
+                    p10 = lds128_if(b1, v);
+                    p11 = lds128_if(b1 + OT, v);
                 } else {
-                    p00 = __ldg(reinterpret_cast<const float4*>(b0));
-                    p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
-                    p10 = __ldg(reinterpret_cast<const float4*>(b1));
-                    p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+                    w = weights_ag(rw[j * Sh::RPW]);
+                    const float* b0 = sh + offs[j];
+                    const float* b1 = b0 + rstride;
+                    if constexpr (kSmemSheet) {
+                        p00 = *reinterpret_cast<const float4*>(b0);
+                        p01 = *reinterpret_cast<const float4*>(b0 + OT);
+                        p10 = *reinterpret_cast<const float4*>(b1);
+                        p11 = *reinterpret_cast<const float4*>(b1 + OT);
+                    } else {
+                        p00 = __ldg(reinterpret_cast<const float4*>(b0));
+                        p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
+                        p10 = __ldg(reinterpret_cast<const float4*>(b1));
+                        p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+                    }
                 }
+                acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
+                acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
+                acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
+                acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
             }
-            acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
-            acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
-            acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
-            acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
         }
         __syncwarp();  // this warp is done with slot u % nbuf (and, at s == S-1, with pair p's records)
         if constexpr (kSmemSheet) {
@@ -547,7 +559,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
         for (int j = 0; j < RT; ++j) {
             const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
-            if (r >= rows) continue;
+            if ((TAIL && !warp_live) || r >= rows) continue;
             XT* yr = base + r * out.ld;
             if constexpr (sizeof(XT) == 4) {
                 if (col + 3 < n_out && y_vec_ok) {

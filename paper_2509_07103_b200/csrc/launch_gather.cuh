@@ -6,11 +6,11 @@
 
 namespace lmkan_b200 {
 
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps, bool TAIL = false>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                            const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW>;
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
     if (!configured[dev]) {
@@ -21,7 +21,7 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
     kern<<<grid, NW * 32, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
                                            static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im, emit,
-                                           emit.W ? *gc_next : L->gc);
+                                           emit.W ? *gc_next : L->gc, static_cast<int>(pl.row_tile));
     return cudaGetLastError();
 }
 
@@ -36,6 +36,15 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
             case 2: return launch_fused_t<OT, 4, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
             case 1: return launch_fused_t<OT, 4, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
             default: break;
+        }
+    }
+    if constexpr (!SLAB) {  // row tiles shortened to fill whole waves of SMs (planner: RT 16 / 8 only)
+        if (pl.row_tile < pl.sh.R) {
+            if (pl.RT == 16)
+                return launch_fused_t<OT, 16, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+                                                                             gc_next, st);
+            return launch_fused_t<OT, 8, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+                                                                        gc_next, st);
         }
     }
     switch (pl.RT) {

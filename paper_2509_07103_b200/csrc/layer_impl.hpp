@@ -29,6 +29,7 @@ struct Plan {
     uint32_t smem;
     int64_t row_tiles, rows_pad;
     int launches;
+    int64_t row_tile;  // rows per CTA tile, <= sh.R (smaller to balance the grid over the SMs)
 };
 
 // Launch the gather kernel variant selected by `pl` for output tile OT

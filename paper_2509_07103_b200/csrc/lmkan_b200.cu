@@ -132,7 +132,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     if (L->narrow) {
         const int64_t ctas = std::min<int64_t>(kNumSMs, (rows + kNarrowThreads - 1) / kNarrowThreads);
         out = Plan{L->OT, 1, 1, kModeNarrow, 1, shape_rt(16, 4), narrow_smem_bytes(L->G, L->pairs, L->OT), ctas,
-                   rows, 1};
+                   rows, 1, 0};
         return static_cast<int>(out.smem) <= smem_cap;
     }
     int force_mode = -1;
@@ -183,8 +183,25 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
                         const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW);
                         if (static_cast<int>(s.total) > smem_cap) continue;
-                        out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, tiles, tiles * sh.R,
-                                   mode == kModeStaged ? 2 : 1};
+                        // Balance: rows per tile Rt <= R so the CTAs fill whole waves of
+                        // the SMs (the last partial wave otherwise idles SMs): cfg4's 128
+                        // CTAs of 2048 rows become 147 of 1792
+                        int64_t Rt = sh.R, nt = tiles;
+                        if (env_int("LMKAN_B200_BALANCE", 1) && RT >= 8 && NW == kWarps && S == 1 &&
+                            mode != kModeGlobal) {
+                            const int64_t ctas = tiles * L->n_ot;
+                            const int64_t waves = (ctas + kNumSMs - 1) / kNumSMs;
+                            const int64_t want = waves * kNumSMs / L->n_ot;
+                            if (want > tiles) {
+                                // whole warps only (a warp is all in or all out of the
+                                // tile: no masked rows in the hot loop); also even
+                                Rt = (rows + want - 1) / want;
+                                Rt = std::min<int64_t>(sh.R, (Rt + sh.ROWS_W - 1) / sh.ROWS_W * sh.ROWS_W);
+                                nt = (rows + Rt - 1) / Rt;
+                            }
+                        }
+                        out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, nt, nt * Rt,
+                                   mode == kModeStaged ? 2 : 1, Rt};
                         return true;
                     }
                 }
@@ -253,8 +270,12 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
         const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
-        records_kernel<XT><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc,
-                                                                            pl.sh, H, recW, recO, im);
+        if (pl.row_tile < pl.sh.R)
+            records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                         im, pl.row_tile);
+        else
+            records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                          im, pl.row_tile);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(recW, st);
@@ -503,6 +524,7 @@ bool chain_fusable(const lmkan_b200_layer* A, const Plan& pa, const lmkan_b200_l
     if (A->n_out != A->n_out_total || B->n_out != B->n_out_total || A->n_out != B->n_in) return false;
     if (pa.mode == kModeNarrow || A->device != B->device) return false;
     if (!make_plan(B, rows, cap, pb) || pb.mode != kModeStaged) return false;
+    if (pa.row_tile != pa.sh.R || pb.row_tile != pb.sh.R) return false;  // the emitter assumes full row tiles
     const lmkan_b200_layer* ls[2] = {A, B};
     const Plan* ps[2] = {&pa, &pb};
     for (int i = 0; i < 2; ++i) {
@@ -930,7 +952,7 @@ int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int*
     if (out_tile) *out_tile = pl.OT;
     if (rows_per_thread) *rows_per_thread = pl.RT;
     if (nbuf) *nbuf = pl.nbuf;
-    if (rows_per_cta_out) *rows_per_cta_out = pl.sh.R;
+    if (rows_per_cta_out) *rows_per_cta_out = static_cast<int>(pl.row_tile > 0 ? pl.row_tile : pl.sh.R);
     if (launches) *launches = pl.launches;
     if (mode) *mode = pl.mode;
     if (slabs) *slabs = pl.S;

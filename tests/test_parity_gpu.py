@@ -406,3 +406,25 @@ def test_conv_argument_errors(torch, pkg):
         layer.conv_forward(torch.zeros((1, 1, 1, 4), device="cuda"), 2, 1)
     with pytest.raises(ValueError, match="expected width 16, got 36"):
         layer.conv_forward(img, 3, 1)
+
+
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+def test_balanced_row_tiles_bitwise(torch, pkg, oracle, monkeypatch, mode):
+    """Row tiles shortened to whole warps so the grid fills the SMs (cfg4-like:
+    128 CTAs of 2048 rows -> 147 of 1792): bitwise equal to the full-tile
+    launch, and within the parity bar of the oracle on a row subset."""
+    n_in, n_out, G, rows = 32, 16, 8, 250000
+    rng = np.random.default_rng(12)
+    P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / 4).astype(np.float32)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    X = torch.randn((rows, n_in), device="cuda")
+    monkeypatch.setenv("LMKAN_B200_MODE", mode)
+    outs = []
+    for bal in ("0", "1"):
+        monkeypatch.setenv("LMKAN_B200_BALANCE", bal)
+        outs.append((layer.plan(rows), layer.forward(X)))
+    (p_full, y_full), (p_bal, y_bal) = outs
+    assert p_bal["rows_per_cta"] < p_full["rows_per_cta"], (p_full, p_bal)
+    assert torch.equal(y_full, y_bal)
+    ref = oracle.forward(G, P.astype(np.float64), X[:400].cpu().numpy().astype(np.float64), 1.0)
+    assert _mixed(y_bal[:400].cpu().numpy(), ref).max() <= TOL
