@@ -4,7 +4,8 @@
 // /root/reference/proj/include/lmkan/) on top of the C-ABI in lmkan_b200.h:
 //   Matrix, require_width          matrix.hpp:11-44
 //   SigmaGrid, build_grid           grid.hpp:33-68
-//   interval_index                  grid.hpp:72-75 (threshold form, bit-exact)
+//   sigma, interval_index, preamble grid.hpp:10-17, 72-101 (index: threshold form, bit-exact)
+//   flops_main_term, param_count    costs.hpp:14-29
 //   LmKanLayer                      layer.hpp:24-61 (same fields and P layout)
 //   default_init_scale, init_layer  layer.hpp:63-86 (bit-identical table)
 //   lmkan_forward                   layer.hpp:108-134 (same signature)
@@ -106,11 +107,39 @@ inline SigmaGrid build_grid(int G) {
     return g;
 }
 
+// grid.hpp:10-17: the percentile-grid generator (host, fp64; NaN propagates).
+inline double sigma(double x) {
+    const double t = std::exp(-std::fabs(x));
+    return x > 0.0 ? 1.0 - 0.5 * t : 0.5 * t;
+}
+
 // grid.hpp:72-75, bit-exact: #{k : x >= t_k} (NaN -> 0).
 inline int interval_index(const SigmaGrid& grid, double x) {
     int i = 0;
     for (double t : grid.thresholds) i += x >= t;
     return i;
+}
+
+// grid.hpp:77-101: cell indices and the four bilinear weights of one 2D
+// argument pair (host, fp64, the reference's operation order).
+struct Preamble {
+    int i1 = 0, i2 = 0;
+    double w00 = 0, w10 = 0, w01 = 0, w11 = 0;
+};
+inline Preamble preamble(const SigmaGrid& grid, double x1, double x2) {
+    Preamble r;
+    r.i1 = interval_index(grid, x1);
+    r.i2 = interval_index(grid, x2);
+    const double a = grid.points[r.i1 + 1] - x1;
+    const double b = x1 - grid.points[r.i1];
+    const double c = grid.points[r.i2 + 1] - x2;
+    const double d = x2 - grid.points[r.i2];
+    const double inv = grid.inv_area(r.i1, r.i2);
+    r.w00 = a * c * inv;
+    r.w10 = b * c * inv;
+    r.w01 = a * d * inv;
+    r.w11 = b * d * inv;
+    return r;
 }
 
 namespace detail {
@@ -215,8 +244,24 @@ private:
     bool frozen_ = false;
 };
 
+// costs.hpp:14-29: main-term FMA count (k^d / d) * n_in * n_out and the
+// 2D table size (G+1)^2 * (n_in/2) * n_out.
+inline std::uint64_t flops_main_term(std::uint64_t n_in, std::uint64_t n_out, unsigned d = 2, unsigned k = 2) {
+    if (d < 1) throw std::invalid_argument("flops_main_term: d must be >= 1");
+    if (k < 2) throw std::invalid_argument("flops_main_term: spline order k must be >= 2");
+    if (n_in % d != 0) throw std::invalid_argument("flops_main_term: d must divide n_in");
+    std::uint64_t kd = 1;
+    for (unsigned i = 0; i < d; ++i) kd *= k;
+    return kd * (n_in / d) * n_out;
+}
+
 // layer.hpp:63-65
 inline double default_init_scale(int n_in) { return 1.0 / std::sqrt(static_cast<double>(n_in / 2)); }
+
+// costs.hpp:25-29
+inline std::uint64_t param_count(const LmKanLayer& layer) {
+    return static_cast<std::uint64_t>(layer.grid.G + 1) * (layer.grid.G + 1) * layer.pairs() * layer.n_out;
+}
 
 // layer.hpp:69-86: same validation, the same N(0, scale^2) table drawn from the
 // same named stream (bit-identical), gamma = 0.

@@ -171,6 +171,26 @@ static void test_determinism_and_cache() {  // test_layer.cpp:228-239 + P edits
     for (std::size_t i = 0; i < Y2.size(); ++i) CHECK(Y2.data()[i] == 0.0);
 }
 
+static void test_grid_helpers() {  // test_grid.cpp:34-48, 166-219 restated
+    CHECK(sigma(0.0) == 0.5);
+    CHECK(std::abs(sigma(-std::log(2.0)) - 0.25) < 1e-15);
+    CHECK(std::abs(sigma(0.1) - 0.5475812909820202) < 1e-15);
+    CHECK(std::isnan(sigma(std::nan(""))));
+    const SigmaGrid g = build_grid(4);
+    const Preamble at_node = preamble(g, g.points[1], g.points[2]);  // one-hot at a node
+    CHECK(at_node.i1 == 1 && at_node.i2 == 2 && std::abs(at_node.w00 - 1.0) < 1e-12);
+    const Preamble mid = preamble(g, 0.5 * (g.points[1] + g.points[2]), 0.5 * (g.points[2] + g.points[3]));
+    CHECK(std::abs(mid.w00 - 0.25) < 1e-12 && std::abs(mid.w11 - 0.25) < 1e-12);
+    std::mt19937_64 r(3);
+    std::normal_distribution<double> n(0.0, 2.0);
+    for (int t = 0; t < 100; ++t) {  // partition of unity
+        const Preamble p = preamble(g, n(r), n(r));
+        CHECK(std::abs(p.w00 + p.w10 + p.w01 + p.w11 - 1.0) <= 1e-12);
+    }
+    CHECK(flops_main_term(1024, 1024) == 2ull * 1024 * 1024);
+    CHECK(param_count(init_layer(4, 3, 4, 1)) == 5ull * 5 * 2 * 3);
+}
+
 static void test_interval_index() {  // test_grid.cpp:108-114
     const SigmaGrid g4 = build_grid(4);
     CHECK(interval_index(g4, 0.1) == 2);
@@ -300,6 +320,7 @@ int main(int argc, char** argv) {
     test_linear_sheets();
     test_determinism_and_cache();
     test_interval_index();
+    test_grid_helpers();
     test_backward();
     if (argc > 1) test_load_model(argv[1]);
     std::printf("test_dropin: %d checks, %d failures\n", g_checks, g_fail);
