@@ -19,6 +19,9 @@ struct lmkan_b200_layer {
     size_t table_bytes = 0;
     double* d_inv = nullptr;
     lmkan_b200::GridConst gc{};
+    // bumped by every mutation after creation (set_gamma): captured CUDA graphs
+    // of a model bake gamma into their kernel parameters and re-capture on change
+    uint64_t version = 0;
 };
 
 namespace lmkan_b200 {

@@ -738,6 +738,7 @@ int lmkan_b200_layer_read_table(const lmkan_b200_layer* L, int pair_begin, int p
 
 int lmkan_b200_layer_set_gamma(lmkan_b200_layer* L, double gamma) {
     if (!L) return fail(LMKAN_B200_EINVAL, "set_gamma: null layer");
+    if (L->gamma != gamma) ++L->version;
     L->gamma = gamma;
     return LMKAN_B200_OK;
 }

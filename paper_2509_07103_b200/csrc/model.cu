@@ -381,6 +381,7 @@ struct lmkan_b200_model {
     std::vector<StreamActs> acts;
     struct GraphEntry {
         int64_t rows;
+        uint64_t versions;  // sum of the layers' mutation counters at capture
         int elem;  // sizeof(XT): f32 and f64 chains on the same buffers are different graphs
         const void* X;
         void* Y;
@@ -518,10 +519,12 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     const bool graphable = graphs_enabled() && st != nullptr &&
                            cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    uint64_t vsum = 0;
+    for (const auto* L : M->layers) vsum += L->version;
     if (graphable) {
         for (auto it = M->graphs.begin(); it != M->graphs.end(); ++it) {
-            if (it->rows == rows && it->elem == static_cast<int>(sizeof(XT)) && it->X == X && it->Y == Y &&
-                it->st == st) {
+            if (it->rows == rows && it->versions == vsum && it->elem == static_cast<int>(sizeof(XT)) && it->X == X &&
+                it->Y == Y && it->st == st) {
                 M->graphs.splice(M->graphs.begin(), M->graphs, it);
                 cudaError_t e = cudaGraphLaunch(M->graphs.front().exec, st);
                 if (e != cudaSuccess) return api::cuda_error(e, "model_infer: graph launch");
@@ -542,7 +545,7 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
     cudaGraphExec_t exec = nullptr;
     if (rc == LMKAN_B200_OK && e_end == cudaSuccess && g &&
         cudaGraphInstantiateWithFlags(&exec, g, cudaGraphInstantiateFlagAutoFreeOnLaunch) == cudaSuccess) {
-        M->graphs.push_front({rows, static_cast<int>(sizeof(XT)), X, Y, st, exec});
+        M->graphs.push_front({rows, vsum, static_cast<int>(sizeof(XT)), X, Y, st, exec});
         if (M->graphs.size() > lmkan_b200_model::kMaxGraphs) {
             cudaGraphExecDestroy(M->graphs.back().exec);
             M->graphs.pop_back();

@@ -243,3 +243,25 @@ def test_lmk1_multichunk_stream(pkg, tmp_path, dtype):
         assert np.array_equal(lay.read_table(pb, pe), want[:, :, pb:pe, :])
     sl = pkg.Layer.load_lmk1(path, 0, out_range=(100, 333))
     assert np.array_equal(sl.read_table(10, 30), want[:, :, 10:30, 100:333])
+
+
+@pytest.mark.gpu
+def test_model_graph_recaptures_after_gamma_change(pkg):
+    """A captured chain bakes gamma into its kernel parameters: changing a
+    layer's gamma must not replay the stale graph."""
+    import torch
+    layers = [pkg.Layer.random(16, 32, 8, seed=1), pkg.Layer.random(32, 8, 8, seed=2)]
+    model = pkg.Model.from_layers(layers)
+    st = torch.cuda.Stream()
+    X = torch.randn((1000, 16), device="cuda")
+    Y = torch.empty((1000, 8), device="cuda")
+    for _ in range(2):
+        with torch.cuda.stream(st):
+            model.infer_into(X, Y, st)
+    st.synchronize()
+    base = Y.clone()
+    layers[1].set_gamma(0.5)
+    with torch.cuda.stream(st):
+        model.infer_into(X, Y, st)
+    st.synchronize()
+    assert torch.allclose(Y, 0.5 * base, rtol=1e-6, atol=1e-7)
