@@ -183,15 +183,17 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
                         const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW);
                         if (static_cast<int>(s.total) > smem_cap) continue;
-                        // Balance: rows per tile Rt <= R so the CTAs fill whole waves of
-                        // the SMs (the last partial wave otherwise idles SMs): cfg4's 128
-                        // CTAs of 2048 rows become 147 of 1792
+                        // Balance: rows per tile Rt <= R so a grid of less than one wave
+                        // fills the SMs: cfg4's 128 CTAs of 2048 rows become 147 of 1792
                         int64_t Rt = sh.R, nt = tiles;
                         if (env_int("LMKAN_B200_BALANCE", 1) && RT >= 8 && NW == kWarps && S == 1 &&
                             mode != kModeGlobal) {
+                            // only a grid of less than one wave: with more waves the tail is
+                            // a small fraction and shortened tiles (less sheet reuse, idle
+                            // warps) cost more than they save (cfg2's chunked host path:
+                            // e2e 19.5 -> 21.0 ms when its 256-CTA chunks were balanced)
                             const int64_t ctas = tiles * L->n_ot;
-                            const int64_t waves = (ctas + kNumSMs - 1) / kNumSMs;
-                            const int64_t want = waves * kNumSMs / L->n_ot;
+                            const int64_t want = ctas < kNumSMs ? kNumSMs / L->n_ot : 0;
                             if (want > tiles) {
                                 // whole warps only (a warp is all in or all out of the
                                 // tile: no masked rows in the hot loop); also even
