@@ -820,7 +820,12 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
     if (!make_plan(L, per_img * N, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
     // at least one full wave of CTAs per chunk, else ~8 chunks
-    const int64_t min_imgs = (static_cast<int64_t>(pl.sh.R) * kNumSMs / std::max(1, L->n_ot) + per_img - 1) / per_img;
+    // chunks of at least one wave of 512-row tiles, so copies overlap kernels (cfg4
+    // e2e: 0.76 ms at 512, 0.81 at 1024, 1.03 as one chunk)
+    // (a full-batch plan's taller tile would otherwise make a single chunk)
+    const int64_t wave_rows = static_cast<int64_t>(env_int("LMKAN_B200_CONV_CHUNK_ROWS", 512)) * kNumSMs /
+                              std::max(1, L->n_ot);
+    const int64_t min_imgs = (wave_rows + per_img - 1) / per_img;
     const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));
     const size_t in_img = static_cast<size_t>(H) * W * C, out_img = static_cast<size_t>(per_img) * L->n_out;
     float* dI[2] = {nullptr, nullptr};
