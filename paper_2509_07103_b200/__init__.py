@@ -303,6 +303,7 @@ class Layer:
                       "warps_per_cta"],
                      [x.value for x in v]))
         d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow"}[d["mode"]]
+        d["lane_vectors"] = int(lib.lmkan_b200_lane_vectors(d["out_tile"]))
         return d
 
     def close(self) -> None:

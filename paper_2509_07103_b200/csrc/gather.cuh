@@ -14,10 +14,22 @@ enum : int {
     kModeNarrow = 3,  // K4: n_out <= 4, whole table resident in shared memory, lanes over pairs
 };
 
+// Float4 runs of outputs per lane. At OT = 64 a lane covers 8 outputs (two
+// float4 runs OT/2 apart), so one warp instruction serves 4 rows instead of 2:
+// each per-row {alpha, gamma} and node-offset load feeds twice the FMAs, and
+// each instruction still reads 4 whole 128-B bank lines. Rows per thread are
+// halved to keep the register tile (RT x V float4 accumulators) and the rows per
+// CTA unchanged. LMKAN_B200_VEC64=1 restores one float4 per lane (A/B builds).
+#ifndef LMKAN_B200_VEC64
+#define LMKAN_B200_VEC64 2
+#endif
+__host__ __device__ constexpr int lane_vectors(int OT) { return OT >= 64 ? LMKAN_B200_VEC64 : 1; }
+
 // Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
 template <int OT, int RT, int NW = kWarps>
 struct FusedShape {
-    static constexpr int LPR = OT / 4;               // lanes covering one row's OT outputs (float4 each)
+    static constexpr int V = lane_vectors(OT);       // float4 runs per lane
+    static constexpr int LPR = OT / (4 * V);         // lanes covering one row's OT outputs
     static constexpr int RPW = 32 / LPR;             // rows per warp per gather instruction
     static constexpr int ROWS_W = RPW * RT;          // rows owned by one warp
     static constexpr int LOC = (ROWS_W + 31) / 32;   // cells each lane locates per pair (fused mode)
@@ -36,7 +48,7 @@ __host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps) {
     s.OT = OT;
     s.RT = RT;
     s.NW = NW;
-    s.LPR = OT / 4;
+    s.LPR = OT / (4 * lane_vectors(OT));
     s.RPW = 32 / s.LPR;
     s.ROWS_W = s.RPW * RT;
     s.R = NW * s.ROWS_W;
@@ -214,10 +226,11 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 //     dedicated to producing.
 //   * fused mode: every warp locates the cells of its own rows for the next pair
 //     into a warp-private record slice (x pair prefetched a pair ahead).
-//   * gather: lane group `sub` handles one row, lane c4 a float4 of outputs; per
-//     row one LDS.64 of {alpha, gamma} (one wavefront for the warp's rows; an
-//     LDS.128 of four weights would cost two) and 4 LDS.128 of coefficients
-//     (nodes n, n+1, n+G+1, n+G+2), 16 FMAs; a lane group's RT node offsets are contiguous
+//   * gather: lane group `sub` handles one row, lane c4 V float4 runs of outputs
+//     (V = lane_vectors(OT)); per row one LDS.64 of {alpha, gamma} (one
+//     wavefront for the warp's rows; an LDS.128 of four weights would cost two)
+//     and 4 V LDS.128 of coefficients (nodes n, n+1, n+G+1, n+G+2), 16 V FMAs;
+//     a lane group's RT node offsets are contiguous
 //     (int4 loads, kept in registers across the pair's slabs). With slabs
 //     (SLAB = true) a row is gathered only during its cell's slab.
 //
@@ -253,7 +266,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    constexpr int V = Sh::V;
+    constexpr int VSTEP = 4 * Sh::LPR;  // floats between a lane's float4 runs
     const int sub = lane / Sh::LPR, c4 = lane % Sh::LPR;
+    // Float offset of the lane's v-th run. Runs of 64 B (V = 4) sit on one bank
+    // half each (a node's 256 B are 128-B aligned); odd lane groups take the runs
+    // in the order 1 0 3 2, so every instruction puts half its rows on each bank
+    // half: 8 rows x 64 B in 4 wavefronts, no conflicts.
+    const int vflip = V >= 4 ? (sub & 1) : 0;
+    auto vofs = [&](int v) { return (v ^ vflip) * VSTEP; };
     const int64_t tile = blockIdx.x;
     // row tiles of Rt <= R rows (Rt < R balances the grid over the SMs): lane
     // slots q >= Rt and rows >= rows are masked, issuing no gathers
@@ -363,9 +384,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     };
 
-    float4 acc[RT];
+    float4 acc[RT][V];
 #pragma unroll
-    for (int j = 0; j < RT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < RT; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[j][v] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int rstride = (G + 1) * OT;  // node (i1+1, i2) is (G+1) nodes further
     // The planner makes Rt a multiple of ROWS_W, so a warp's rows are all inside
     // the tile or all beyond it: warps beyond it issue no gathers. Rows past the
@@ -395,49 +418,62 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const int rs = MODE == kModeStaged ? p % L.nrec : 0;
             rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
             const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
+            if constexpr (RT % 4 == 0) {
 #pragma unroll
-            for (int k = 0; k < RT / 4; ++k) {
-                const int4 v = reinterpret_cast<const int4*>(ro)[k];
-                offs[4 * k] = v.x;
-                offs[4 * k + 1] = v.y;
-                offs[4 * k + 2] = v.z;
-                offs[4 * k + 3] = v.w;
+                for (int k = 0; k < RT / 4; ++k) {
+                    const int4 v = reinterpret_cast<const int4*>(ro)[k];
+                    offs[4 * k] = v.x;
+                    offs[4 * k + 1] = v.y;
+                    offs[4 * k + 2] = v.z;
+                    offs[4 * k + 3] = v.w;
+                }
+            } else if constexpr (RT == 2) {  // small-batch CTAs at V = 2: OSTRIDE = 6, 8-B aligned runs
+                const int2 v = *reinterpret_cast<const int2*>(ro);
+                offs[0] = v.x;
+                offs[1] = v.y;
+            } else {
+                static_assert(RT == 1, "rows per thread: 1, 2 or a multiple of 4");
+                offs[0] = ro[0];
             }
         }
         if (!TAIL || warp_live) {  // TAIL: shortened row tiles, some warps hold no rows
 #pragma unroll
             for (int j = 0; j < RT; ++j) {
-                float4 w, p00, p01, p10, p11;
                 if constexpr (SLAB) {
                     // rows whose cell lies in another slab load nothing and add +0
-                    const bool v = (offs[j] >> kSlabShift) == s;
+                    const bool ok = (offs[j] >> kSlabShift) == s;
                     const float* b0 = sh + (offs[j] & kOffMask);
                     const float* b1 = b0 + rstride;
-                    w = weights_ag(lds64_if(rw + j * Sh::RPW, v));
-                    p00 = lds128_if(b0, v);
-                    p01 = lds128_if(b0 + OT, v);
-                    p10 = lds128_if(b1, v);
-                    p11 = lds128_if(b1 + OT, v);
+                    const float4 w = weights_ag(lds64_if(rw + j * Sh::RPW, ok));
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const float4 p00 = lds128_if(b0 + vofs(v), ok);
+                        const float4 p01 = lds128_if(b0 + vofs(v) + OT, ok);
+                        const float4 p10 = lds128_if(b1 + vofs(v), ok);
+                        const float4 p11 = lds128_if(b1 + vofs(v) + OT, ok);
+                        fma_corners(acc[j][v], w, p00, p10, p01, p11);
+                    }
                 } else {
-                    w = weights_ag(rw[j * Sh::RPW]);
+                    const float4 w = weights_ag(rw[j * Sh::RPW]);
                     const float* b0 = sh + offs[j];
                     const float* b1 = b0 + rstride;
-                    if constexpr (kSmemSheet) {
-                        p00 = *reinterpret_cast<const float4*>(b0);
-                        p01 = *reinterpret_cast<const float4*>(b0 + OT);
-                        p10 = *reinterpret_cast<const float4*>(b1);
-                        p11 = *reinterpret_cast<const float4*>(b1 + OT);
-                    } else {
-                        p00 = __ldg(reinterpret_cast<const float4*>(b0));
-                        p01 = __ldg(reinterpret_cast<const float4*>(b0 + OT));
-                        p10 = __ldg(reinterpret_cast<const float4*>(b1));
-                        p11 = __ldg(reinterpret_cast<const float4*>(b1 + OT));
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        float4 p00, p01, p10, p11;
+                        if constexpr (kSmemSheet) {
+                            p00 = *reinterpret_cast<const float4*>(b0 + vofs(v));
+                            p01 = *reinterpret_cast<const float4*>(b0 + vofs(v) + OT);
+                            p10 = *reinterpret_cast<const float4*>(b1 + vofs(v));
+                            p11 = *reinterpret_cast<const float4*>(b1 + vofs(v) + OT);
+                        } else {
+                            p00 = __ldg(reinterpret_cast<const float4*>(b0 + vofs(v)));
+                            p01 = __ldg(reinterpret_cast<const float4*>(b0 + vofs(v) + OT));
+                            p10 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v)));
+                            p11 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v) + OT));
+                        }
+                        fma_corners(acc[j][v], w, p00, p10, p01, p11);
                     }
                 }
-                acc[j].x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
-                acc[j].y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
-                acc[j].z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
-                acc[j].w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
             }
         }
         __syncwarp();  // this warp is done with slot u % nbuf (and, at s == S-1, with pair p's records)
@@ -472,15 +508,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // epilogue: y *= gamma (layer.hpp:131), masked store of the warp's rows into
     // every destination (peer destinations are NVLink stores issued as the
     // CTA's tile completes, overlapping the other CTAs' gathers)
-    const int col = ot * OT + 4 * c4;
+    const int col = ot * OT + 4 * c4;  // run v holds outputs col + vofs(v) .. + 3
 #pragma unroll
-    for (int j = 0; j < RT; ++j) acc[j] = make_float4(acc[j].x * gamma, acc[j].y * gamma, acc[j].z * gamma,
-                                                      acc[j].w * gamma);
+    for (int j = 0; j < RT; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            acc[j][v] = make_float4(acc[j][v].x * gamma, acc[j][v].y * gamma, acc[j][v].z * gamma, acc[j][v].w * gamma);
     if constexpr (sizeof(XT) == 4) {
         if (emit.W) {
-            // fused chain: this lane's outputs col..col+3 are the next layer's pairs
-            // col/2 and col/2 + 1. Two passes (h = 0, 1), one next-layer pair per lane
-            // each: locate into shared memory [pair][row], then coalesced record
+            // fused chain: the lane's outputs cv..cv+3 of each run (cv = col + vofs(v))
+            // are the next layer's pairs cv/2 and cv/2 + 1. Two passes (h = 0, 1), one
+            // next-layer pair per run each: locate into shared memory [pair][row], then coalesced record
             // stores — rows run contiguously in W, and when both layers use the same
             // row tile the CTA's offset block of each pair is written whole.
             constexpr int PP = OT / 4;  // next-layer pairs per pass
@@ -507,14 +545,19 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 for (int j = 0; j < RT; ++j) {
                     const int rl = warp * Sh::ROWS_W + j * Sh::RPW + sub;
                     const int64_t r = row0 + rl;
-                    float2 ag = make_float2(0.f, 0.f);
-                    int packed = 0;
-                    if (r < rows && col + 2 * h + 1 < n_out) {
-                        const float a = h ? acc[j].z : acc[j].x, b = h ? acc[j].w : acc[j].y;
-                        packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.OT, emit.H, ag);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        float2 ag = make_float2(0.f, 0.f);
+                        int packed = 0;
+                        if (r < rows && col + vofs(v) + 2 * h + 1 < n_out) {
+                            const float a = h ? acc[j][v].z : acc[j][v].x, b = h ? acc[j][v].w : acc[j][v].y;
+                            packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.OT,
+                                                      emit.H, ag);
+                        }
+                        const int cv = (v ^ vflip) * Sh::LPR + c4;  // (col + vofs(v) - ot OT) / 4
+                        sW[cv * R + rl] = ag;
+                        sO[cv * R + rl] = packed;
                     }
-                    sW[c4 * R + rl] = ag;
-                    sO[c4 * R + rl] = packed;
                 }
                 __syncthreads();
                 for (int idx = tid; idx < PP * R; idx += NT) {
@@ -561,16 +604,20 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const int64_t r = row0 + warp * Sh::ROWS_W + j * Sh::RPW + sub;
             if ((TAIL && !warp_live) || r >= rows) continue;
             XT* yr = base + r * out.ld;
-            if constexpr (sizeof(XT) == 4) {
-                if (col + 3 < n_out && y_vec_ok) {
-                    *reinterpret_cast<float4*>(yr + col) = acc[j];
-                    continue;
-                }
-            }
-            const float v[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (col + e < n_out) yr[col + e] = static_cast<XT>(v[e]);
+            for (int v = 0; v < V; ++v) {
+                const int cv = col + vofs(v);
+                if constexpr (sizeof(XT) == 4) {
+                    if (cv + 3 < n_out && y_vec_ok) {
+                        *reinterpret_cast<float4*>(yr + cv) = acc[j][v];
+                        continue;
+                    }
+                }
+                const float a[4] = {acc[j][v].x, acc[j][v].y, acc[j][v].z, acc[j][v].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (cv + e < n_out) yr[cv + e] = static_cast<XT>(a[e]);
+            }
         }
     }
 }

@@ -29,29 +29,30 @@ template <int OT, typename XT, int MODE, bool SLAB>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                             const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
-    if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT = 4) so the grid still spans the GPU
+    // rows per thread: the planner's {16, 8, 4} float4 accumulators per thread / V
+    constexpr int V = lane_vectors(OT);
+    constexpr int RT0 = 16 / V, RT1 = 8 / V, RT2 = 4 / V;
+    if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT2) so the grid still spans the GPU
         switch (pl.sh.NW) {
-            case 8: return launch_fused_t<OT, 4, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 4: return launch_fused_t<OT, 4, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 2: return launch_fused_t<OT, 4, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 1: return launch_fused_t<OT, 4, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 8: return launch_fused_t<OT, RT2, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 4: return launch_fused_t<OT, RT2, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 2: return launch_fused_t<OT, RT2, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 1: return launch_fused_t<OT, RT2, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
             default: break;
         }
     }
-    if constexpr (!SLAB) {  // row tiles shortened to fill whole waves of SMs (planner: RT 16 / 8 only)
+    if constexpr (!SLAB) {  // row tiles shortened to fill whole waves of SMs (planner: RT0 / RT1 only)
         if (pl.row_tile < pl.sh.R) {
-            if (pl.RT == 16)
-                return launch_fused_t<OT, 16, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
-                                                                             gc_next, st);
-            return launch_fused_t<OT, 8, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
-                                                                        gc_next, st);
+            if (pl.RT == RT0)
+                return launch_fused_t<OT, RT0, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+                                                                              gc_next, st);
+            return launch_fused_t<OT, RT1, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+                                                                          gc_next, st);
         }
     }
-    switch (pl.RT) {
-        case 16: return launch_fused_t<OT, 16, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-        case 8: return launch_fused_t<OT, 8, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-        default: return launch_fused_t<OT, 4, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-    }
+    if (pl.RT == RT0) return launch_fused_t<OT, RT0, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    if (pl.RT == RT1) return launch_fused_t<OT, RT1, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    return launch_fused_t<OT, RT2, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
 }
 
 template <int OT, typename XT>
@@ -59,7 +60,7 @@ cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X
                               const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
     if (pl.mode == kModeGlobal)
-        return launch_fused_t<OT, 4, XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+        return launch_fused_t<OT, 4 / lane_vectors(OT), XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
     if (pl.mode == kModeStaged)
         return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
                         : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);

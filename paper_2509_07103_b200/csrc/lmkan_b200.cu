@@ -86,6 +86,8 @@ int max_smem_optin(int device) {
 }
 
 // ---------------------------------------------------------------- planning
+// float4 accumulators per thread (the register tile); rows per thread RT =
+// choice / lane_vectors(OT), so the rows per CTA do not depend on V
 constexpr int kRTChoices[] = {16, 8, 4};
 constexpr int kNumSMs = 148;
 constexpr int kMaxSlabs = 4;
@@ -108,8 +110,8 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
         for (int S = 1; S <= (want_buf == 2 ? 3 : 1); ++S) {
             for (int OT : {64, 32, 16}) {
                 if (OT > 16 && OT / 2 >= n_out) continue;
-                for (int RT : kRTChoices) {
-                    const FusedSmem s = fused_smem_layout(G, OT, RT, want_buf, kModeStaged, S);
+                for (int A : kRTChoices) {
+                    const FusedSmem s = fused_smem_layout(G, OT, A / lane_vectors(OT), want_buf, kModeStaged, S);
                     if (static_cast<int>(s.total) <= smem_cap) return OT;
                 }
             }
@@ -144,8 +146,8 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     // staged when >= 3 output tiles re-read the cells, or when the batch is too
     // small to give every SM a 16-warp CTA (the per-pair locate then sits on the
     // critical path of the few rows each CTA owns; measured 32 vs 47 us at cfg1)
-    const bool small = ((rows + shape_rt(L->OT, kRTChoices[2]).R - 1) / shape_rt(L->OT, kRTChoices[2]).R) * L->n_ot <
-                       kNumSMs;
+    const int rt_small = kRTChoices[2] / lane_vectors(L->OT);
+    const bool small = ((rows + shape_rt(L->OT, rt_small).R - 1) / shape_rt(L->OT, rt_small).R) * L->n_ot < kNumSMs;
     const int pref = (L->n_ot >= 3 || small) ? kModeStaged : kModeFused;
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
     for (int mode : modes) {
@@ -156,12 +158,14 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
             for (int S = 1; S <= (smem_sheet ? kMaxSlabs : 1); ++S) {
                 if (force_s && S != force_s) continue;
                 if (S > 1 && min_buf == 1) continue;
-                for (int RT : kRTChoices) {
+                for (int A : kRTChoices) {
+                    const int RT = A / lane_vectors(L->OT);
                     if (force_rt && RT != force_rt) continue;
+                    if (mode == kModeGlobal && A != kRTChoices[2]) continue;  // the global-sheet kernel is built for RT2 only
                     // warps per CTA: 16, or for batches too small to give every SM a
                     // 16-warp CTA at RT = 4, the largest of {8, 4, 2, 1} that does
                     int NW = kWarps;
-                    if (RT == kRTChoices[2] && S == 1 && mode != kModeGlobal) {
+                    if (A == kRTChoices[2] && S == 1 && mode != kModeGlobal) {
                         const int force_nw = env_int("LMKAN_B200_NW", 0);
                         if (force_nw) {
                             NW = force_nw;
@@ -176,7 +180,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                     // a taller row tile reuses each sheet for more rows; take it while the
                     // grid still covers >= 3/4 of the SMs (cfg4: RT 16 with 128 CTAs 0.392 ms
                     // beat RT 8 with 256 CTAs = 1.7 waves, 0.404 ms)
-                    if (!force_rt && RT != kRTChoices[2] && tiles * L->n_ot * 4 < kNumSMs * 3) continue;
+                    if (!force_rt && A != kRTChoices[2] && tiles * L->n_ot * 4 < kNumSMs * 3) continue;
                     for (int nbuf = smem_sheet ? max_nbuf : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
@@ -186,7 +190,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         // Balance: rows per tile Rt <= R so a grid of less than one wave
                         // fills the SMs: cfg4's 128 CTAs of 2048 rows become 147 of 1792
                         int64_t Rt = sh.R, nt = tiles;
-                        if (env_int("LMKAN_B200_BALANCE", 1) && RT >= 8 && NW == kWarps && S == 1 &&
+                        if (env_int("LMKAN_B200_BALANCE", 1) && A >= 8 && NW == kWarps && S == 1 &&
                             mode != kModeGlobal) {
                             // only a grid of less than one wave: with more waves the tail is
                             // a small fraction and shortened tiles (less sheet reuse, idle
@@ -951,6 +955,8 @@ int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i
                           int64_t rows, void* stream) {
     return locate_device<double>(L, X, i1, i2, w, rows, static_cast<cudaStream_t>(stream));
 }
+
+int lmkan_b200_lane_vectors(int out_tile) { return lane_vectors(out_tile); }
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
                     int* rows_per_cta_out, int* launches, int* mode, int* slabs, int* warps_per_cta) {

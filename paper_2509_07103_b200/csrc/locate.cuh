@@ -137,4 +137,14 @@ __device__ __forceinline__ float4 weights_ag(float2 ag) {
     return make_float4(ag.x * ag.y, b * ag.y, ag.x * d, b * d);
 }
 
+// acc += ((w00 p00 + w10 p10) + w01 p01) + w11 p11 per output, fused
+// multiply-adds in the reference's per-pair grouping (layer.hpp:129).
+__device__ __forceinline__ void fma_corners(float4& acc, const float4 w, const float4 p00, const float4 p10,
+                                            const float4 p01, const float4 p11) {
+    acc.x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
+    acc.y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
+    acc.z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
+    acc.w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
+}
+
 }  // namespace lmkan_b200

@@ -239,7 +239,9 @@ def test_f64_device_path(torch, pkg, oracle):
 
 
 VARIANTS = [("fused", "1", "16"), ("fused", "2", "8"), ("fused", "3", "4"), ("staged", "1", "16"),
-            ("staged", "2", "16"), ("staged", "3", "8"), ("staged", "4", "4"), ("global", "1", "4")]
+            ("staged", "2", "16"), ("staged", "3", "8"), ("staged", "4", "4"), ("global", "1", "4"),
+            # OT = 64 runs two float4 runs per lane: rows per thread 8 / 4 / 2
+            ("staged", "1", "2"), ("fused", "2", "2"), ("global", "1", "2")]
 
 
 @pytest.mark.parametrize("G", [8, 28, 32])
@@ -277,7 +279,7 @@ def test_kernel_variants_parity_and_bitwise_agreement(torch, pkg, oracle, monkey
 
 @pytest.mark.parametrize("ot", ["64", "16"])
 def test_small_batch_warps_per_cta(torch, pkg, oracle, monkeypatch, ot):
-    """Small batches run CTAs of 8/4/2/1 warps (RT = 4) so the grid spans the
+    """Small batches run CTAs of 8/4/2/1 warps (4 float4s per thread) so the grid spans the
     GPU; every warps-per-CTA choice meets the parity bar and is bitwise equal
     to the 16-warp launch (the per-row summation order does not change)."""
     n_in, n_out, G, rows = 64, 64, 8, 1024  # config 1
@@ -290,11 +292,12 @@ def test_small_batch_warps_per_cta(torch, pkg, oracle, monkeypatch, ot):
     ctas = -(-rows // auto["rows_per_cta"]) * -(-n_out // auto["out_tile"])
     assert auto["warps_per_cta"] < 16 and (ctas >= 148 or auto["warps_per_cta"] == 1), auto
     outs = []
+    small_rt = str(4 // auto["lane_vectors"])  # the small-batch register tile: 4 float4s per thread
     for mode in ("fused", "staged"):
         monkeypatch.setenv("LMKAN_B200_MODE", mode)
         for nw in ("16", "8", "4", "2", "1"):
             monkeypatch.setenv("LMKAN_B200_NW", nw)
-            monkeypatch.setenv("LMKAN_B200_RT", "4")
+            monkeypatch.setenv("LMKAN_B200_RT", small_rt)
             plan = layer.plan(rows)
             assert plan["warps_per_cta"] == int(nw) and plan["mode"] == mode, plan
             Y = layer.forward(Xd)
