@@ -14,16 +14,25 @@ enum : int {
     kModeNarrow = 3,  // K4: n_out <= 4, whole table resident in shared memory, lanes over pairs
 };
 
-// Float4 runs of outputs per lane. At OT = 64 a lane covers 8 outputs (two
-// float4 runs OT/2 apart), so one warp instruction serves 4 rows instead of 2:
-// each per-row {alpha, gamma} and node-offset load feeds twice the FMAs, and
-// each instruction still reads 4 whole 128-B bank lines. Rows per thread are
-// halved to keep the register tile (RT x V float4 accumulators) and the rows per
-// CTA unchanged. LMKAN_B200_VEC64=1 restores one float4 per lane (A/B builds).
+// Float4 runs of outputs per lane. At OT = 64 a lane covers 16 outputs (four
+// float4 runs OT/4 apart), so one warp instruction serves 8 rows instead of 2:
+// each per-row {alpha, gamma} and node-offset load feeds 4x the FMAs, and the
+// bank-half interleave in fwd_fused_kernel keeps each instruction at 4
+// wavefronts. Rows per thread shrink by V to keep the register tile (RT x V
+// float4 accumulators) and the rows per CTA unchanged. Same-box A/B at cfg2
+// (K2 ms): V = 1 18.12, V = 2 17.35, V = 4 17.00. LMKAN_B200_VEC64 = 1 / 2
+// selects the others (A/B builds).
+// At OT = 32 likewise two runs (8 rows per instruction); OT = 16 keeps one
+// run per lane and gets its conflict-free loads from duplicated nodes (DUP).
 #ifndef LMKAN_B200_VEC64
-#define LMKAN_B200_VEC64 2
+#define LMKAN_B200_VEC64 4
 #endif
-__host__ __device__ constexpr int lane_vectors(int OT) { return OT >= 64 ? LMKAN_B200_VEC64 : 1; }
+#ifndef LMKAN_B200_VEC32
+#define LMKAN_B200_VEC32 2
+#endif
+__host__ __device__ constexpr int lane_vectors(int OT) {
+    return OT >= 64 ? LMKAN_B200_VEC64 : (OT == 32 ? LMKAN_B200_VEC32 : 1);
+}
 
 // Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
 template <int OT, int RT, int NW = kWarps>
@@ -37,15 +46,17 @@ struct FusedShape {
     static constexpr int OSTRIDE = RT + (RPW > 2 ? 4 : 0);  // padded per-lane-group offset run (bank spread)
     static constexpr int OBLK = NW * RPW * OSTRIDE;         // offset ints per CTA per pair
 };
-// Runtime twin of FusedShape for host code / K1.
+// Runtime twin of FusedShape for host code / K1. NS = the table's node stride
+// in floats: OT, or 2 OT for a duplicated-node (DUP) table (see fwd_fused_kernel).
 struct ShapeRT {
-    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK, NW;
+    int OT, RT, LPR, RPW, ROWS_W, R, OSTRIDE, OBLK, NW, NS;
     int lgRPW, lgROWS_W, lgR;  // RPW, ROWS_W, R are powers of two (OT, RT, NW are)
 };
 __host__ __device__ constexpr int ilog2(int v) { return v > 1 ? 1 + ilog2(v >> 1) : 0; }
-__host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps) {
+__host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps, int NS = 0) {
     ShapeRT s;
     s.OT = OT;
+    s.NS = NS > 0 ? NS : OT;
     s.RT = RT;
     s.NW = NW;
     s.LPR = OT / (4 * lane_vectors(OT));
@@ -103,13 +114,13 @@ struct FusedSmem {
     int nrec;
 };
 __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1,
-                                                       int NW = kWarps) {
+                                                       int NW = kWarps, int NS = 0) {
     const ShapeRT sh = shape_rt(OT, RT, NW);
     const int H = (G + S - 1) / S;
     const int nb = nbuf > 0 ? nbuf : 1;
     FusedSmem s;
     s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
-    s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * OT * 4u;
+    s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * (NS > 0 ? NS : OT) * 4u;
     s.recw_bytes = sh.R * 8u;  // float2 {alpha, gamma} per row
     s.reco_bytes = sh.OBLK * 4u;
     uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
                     float2 ag = make_float2(0.f, 0.f);
                     int packed = 0;
                     if (g < rows)
-                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.OT, H, ag);
+                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag);
                     *wp = ag;
                     *op = packed;
                 }
@@ -233,12 +244,18 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 //     a lane group's RT node offsets are contiguous
 //     (int4 loads, kept in registers across the pair's slabs). With slabs
 //     (SLAB = true) a row is gathered only during its cell's slab.
+//   * DUP (OT = 16): the table stores every node's 16 outputs twice, side by
+//     side in one 128-B line ([node][copy][OT], node stride NS = 2 OT), and odd
+//     lane groups read the second copy. A 64-B run otherwise sits on the bank
+//     half its node's parity picks, so the 8 rows of an instruction collide on a
+//     half ~27% of the time; with the copies every instruction puts 4 rows on
+//     each half: 4 wavefronts, no conflicts, for twice the sheet bytes.
 //
 // Accumulation order per (row, output): acc = 0; for p: acc += t_p with
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW, bool TAIL>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW, bool TAIL, bool DUP>
 __global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
@@ -250,11 +267,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int Rt = TAIL ? Rt_arg : R;  // full-tile kernels keep the row tile a compile-time constant
     constexpr int NT = NW * 32;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
+    constexpr int NS = DUP ? 2 * OT : OT;  // node stride in the table / sheets (floats)
+    static_assert(!DUP || (!SLAB && MODE != kModeGlobal && lane_vectors(OT) == 1), "DUP: unslabbed smem sheets");
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
     const int H = (G + S - 1) / S;
-    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW);
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW, NS);
     float* sheets = reinterpret_cast<float*>(smem);
     float2* rec_w = reinterpret_cast<float2*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
@@ -269,20 +288,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr int V = Sh::V;
     constexpr int VSTEP = 4 * Sh::LPR;  // floats between a lane's float4 runs
     const int sub = lane / Sh::LPR, c4 = lane % Sh::LPR;
-    // Float offset of the lane's v-th run. Runs of 64 B (V = 4) sit on one bank
-    // half each (a node's 256 B are 128-B aligned); odd lane groups take the runs
-    // in the order 1 0 3 2, so every instruction puts half its rows on each bank
+    // Float offset of the lane's v-th run. Runs of 64 B (OT / V = 16) sit on one
+    // bank half each (nodes are 128-B aligned); odd lane groups take the runs in
+    // the order 1 0 3 2, so every instruction puts half its rows on each bank
     // half: 8 rows x 64 B in 4 wavefronts, no conflicts.
-    const int vflip = V >= 4 ? (sub & 1) : 0;
+    const int vflip = (V >= 2 && VSTEP == 16) ? (sub & 1) : 0;
     auto vofs = [&](int v) { return (v ^ vflip) * VSTEP; };
+    const int lane_base = 4 * c4 + (DUP ? (sub & 1) * OT : 0);  // DUP: odd lane groups read the second copy
     const int64_t tile = blockIdx.x;
     // row tiles of Rt <= R rows (Rt < R balances the grid over the SMs): lane
     // slots q >= Rt and rows >= rows are masked, issuing no gathers
     const int64_t row0 = tile * Rt;
     const int ot = blockIdx.y;
-    const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
-    const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * OT;
-    const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * OT;  // slab stride within a sheet
+    const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * NS;
+    const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * NS;
+    const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * NS;  // slab stride within a sheet
     const int64_t tiles = rows_pad / Rt;
     const uint32_t recw_copy = static_cast<uint32_t>(Rt) * 8u;  // this tile's records (<= L.recw_bytes)
     const int units = pairs * S;
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     auto issue = [&](int u) {  // one thread: slab (+ the pair's records when staged) of unit u
         const int p = u / S, s = u - p * S;
         const int slot = u % nbuf;
-        const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * OT * 4u;
+        const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * NS * 4u;
         const bool with_rec = MODE == kModeStaged && s == 0;
         mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? recw_copy + L.reco_bytes : 0u));
         const char* src =
@@ -369,14 +389,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     };
     auto locate = [&]() {
-        const ShapeRT shp = shape_rt(OT, RT, NW);
+        const ShapeRT shp = shape_rt(OT, RT, NW, NS);
 #pragma unroll
         for (int k = 0; k < Sh::LOC; ++k) {
             const int q = k * 32 + lane;
             if (q < Sh::ROWS_W) {
                 float2 ag = make_float2(0.f, 0.f);
                 int packed = 0;
-                if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, OT, H, ag);
+                if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, NS, H, ag);
                 const int qc = warp * Sh::ROWS_W + q;
                 rec_w[qc] = ag;
                 rec_o[offset_slot(shp, qc)] = packed;
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int j = 0; j < RT; ++j)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[j][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int rstride = (G + 1) * OT;  // node (i1+1, i2) is (G+1) nodes further
+    const int rstride = (G + 1) * NS;  // node (i1+1, i2) is (G+1) nodes further
     // The planner makes Rt a multiple of ROWS_W, so a warp's rows are all inside
     // the tile or all beyond it: warps beyond it issue no gathers. Rows past the
     // batch end inside the last tile gather zero-weight records (no branch in
@@ -410,9 +430,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if constexpr (kSmemSheet) {
             const int slot = u % nbuf;
             mbar_wait(&full[slot], static_cast<uint32_t>((u / nbuf) & 1));
-            sh = sheets + static_cast<size_t>(slot) * (L.sheet_bytes / 4) + 4 * c4;
+            sh = sheets + static_cast<size_t>(slot) * (L.sheet_bytes / 4) + lane_base;
         } else {
-            sh = tsrc + static_cast<size_t>(p) * sheet_floats + 4 * c4;
+            sh = tsrc + static_cast<size_t>(p) * sheet_floats + lane_base;
         }
         if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets to registers (kept across slabs)
             const int rs = MODE == kModeStaged ? p % L.nrec : 0;
@@ -448,9 +468,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         const float4 p00 = lds128_if(b0 + vofs(v), ok);
-                        const float4 p01 = lds128_if(b0 + vofs(v) + OT, ok);
+                        const float4 p01 = lds128_if(b0 + vofs(v) + NS, ok);
                         const float4 p10 = lds128_if(b1 + vofs(v), ok);
-                        const float4 p11 = lds128_if(b1 + vofs(v) + OT, ok);
+                        const float4 p11 = lds128_if(b1 + vofs(v) + NS, ok);
                         fma_corners(acc[j][v], w, p00, p10, p01, p11);
                     }
                 } else {
@@ -462,14 +482,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         float4 p00, p01, p10, p11;
                         if constexpr (kSmemSheet) {
                             p00 = *reinterpret_cast<const float4*>(b0 + vofs(v));
-                            p01 = *reinterpret_cast<const float4*>(b0 + vofs(v) + OT);
+                            p01 = *reinterpret_cast<const float4*>(b0 + vofs(v) + NS);
                             p10 = *reinterpret_cast<const float4*>(b1 + vofs(v));
-                            p11 = *reinterpret_cast<const float4*>(b1 + vofs(v) + OT);
+                            p11 = *reinterpret_cast<const float4*>(b1 + vofs(v) + NS);
                         } else {
                             p00 = __ldg(reinterpret_cast<const float4*>(b0 + vofs(v)));
-                            p01 = __ldg(reinterpret_cast<const float4*>(b0 + vofs(v) + OT));
+                            p01 = __ldg(reinterpret_cast<const float4*>(b0 + vofs(v) + NS));
                             p10 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v)));
-                            p11 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v) + OT));
+                            p11 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v) + NS));
                         }
                         fma_corners(acc[j][v], w, p00, p10, p01, p11);
                     }
@@ -551,7 +571,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         int packed = 0;
                         if (r < rows && col + vofs(v) + 2 * h + 1 < n_out) {
                             const float a = h ? acc[j][v].z : acc[j][v].x, b = h ? acc[j][v].w : acc[j][v].y;
-                            packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.OT,
+                            packed = locate_ag<float>(a, b, nthr, npts, ninv, gc_next.G, gc_next.L, emit.sh.NS,
                                                       emit.H, ag);
                         }
                         const int cv = (v ^ vflip) * Sh::LPR + c4;  // (col + vofs(v) - ot OT) / 4

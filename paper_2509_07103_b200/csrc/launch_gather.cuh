@@ -6,11 +6,11 @@
 
 namespace lmkan_b200 {
 
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps, bool TAIL = false>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps, bool TAIL = false, bool DUP = false>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                            const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL>;
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL, DUP>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
     if (!configured[dev]) {
@@ -25,7 +25,7 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
     return cudaGetLastError();
 }
 
-template <int OT, typename XT, int MODE, bool SLAB>
+template <int OT, typename XT, int MODE, bool SLAB, bool DUP = false>
 cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                             const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
@@ -34,50 +34,58 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
     constexpr int RT0 = 16 / V, RT1 = 8 / V, RT2 = 4 / V;
     if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT2) so the grid still spans the GPU
         switch (pl.sh.NW) {
-            case 8: return launch_fused_t<OT, RT2, XT, MODE, false, 8>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 4: return launch_fused_t<OT, RT2, XT, MODE, false, 4>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 2: return launch_fused_t<OT, RT2, XT, MODE, false, 2>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-            case 1: return launch_fused_t<OT, RT2, XT, MODE, false, 1>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 8: return launch_fused_t<OT, RT2, XT, MODE, false, 8, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 4: return launch_fused_t<OT, RT2, XT, MODE, false, 4, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 2: return launch_fused_t<OT, RT2, XT, MODE, false, 2, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+            case 1: return launch_fused_t<OT, RT2, XT, MODE, false, 1, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
             default: break;
         }
     }
     if constexpr (!SLAB) {  // row tiles shortened to fill whole waves of SMs (planner: RT0 / RT1 only)
         if (pl.row_tile < pl.sh.R) {
             if (pl.RT == RT0)
-                return launch_fused_t<OT, RT0, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+                return launch_fused_t<OT, RT0, XT, MODE, false, kWarps, true, DUP>(L, pl, X, Y, rows, recW, recO, im, emit,
                                                                               gc_next, st);
-            return launch_fused_t<OT, RT1, XT, MODE, false, kWarps, true>(L, pl, X, Y, rows, recW, recO, im, emit,
+            return launch_fused_t<OT, RT1, XT, MODE, false, kWarps, true, DUP>(L, pl, X, Y, rows, recW, recO, im, emit,
                                                                           gc_next, st);
         }
     }
-    if (pl.RT == RT0) return launch_fused_t<OT, RT0, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-    if (pl.RT == RT1) return launch_fused_t<OT, RT1, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-    return launch_fused_t<OT, RT2, XT, MODE, SLAB>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    if (pl.RT == RT0) return launch_fused_t<OT, RT0, XT, MODE, SLAB, kWarps, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    if (pl.RT == RT1) return launch_fused_t<OT, RT1, XT, MODE, SLAB, kWarps, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    return launch_fused_t<OT, RT2, XT, MODE, SLAB, kWarps, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
 }
 
-template <int OT, typename XT>
+template <int OT, typename XT, bool DUP>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                               const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
-    if (pl.mode == kModeGlobal)
-        return launch_fused_t<OT, 4 / lane_vectors(OT), XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-    if (pl.mode == kModeStaged)
-        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
-                        : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
-    return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
-                    : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    if constexpr (DUP) {  // duplicated-node tables: unslabbed shared-memory sheets only (planner)
+        if (pl.mode == kModeGlobal || pl.S > 1) return cudaErrorInvalidConfiguration;
+        return pl.mode == kModeStaged
+                   ? launch_fused_rt<OT, XT, kModeStaged, false, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
+                   : launch_fused_rt<OT, XT, kModeFused, false, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    } else {
+        if (pl.mode == kModeGlobal)
+            return launch_fused_t<OT, 4 / lane_vectors(OT), XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im,
+                                                                                   emit, gc_next, st);
+        if (pl.mode == kModeStaged)
+            return pl.S > 1 ? launch_fused_rt<OT, XT, kModeStaged, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
+                            : launch_fused_rt<OT, XT, kModeStaged, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+        return pl.S > 1 ? launch_fused_rt<OT, XT, kModeFused, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
+                        : launch_fused_rt<OT, XT, kModeFused, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
+    }
 }
 
 }  // namespace lmkan_b200
 
-#define LMKAN_B200_INSTANTIATE_GATHER(OT)                                                                        \
-    template cudaError_t lmkan_b200::launch_gather<OT, float>(const lmkan_b200_layer*, const lmkan_b200::Plan&, \
+#define LMKAN_B200_INSTANTIATE_GATHER(OT, DUP)                                                                   \
+    template cudaError_t lmkan_b200::launch_gather<OT, float, DUP>(const lmkan_b200_layer*, const lmkan_b200::Plan&, \
                                                               const float*, const lmkan_b200::OutDests<float>&, \
                                                               int64_t, const float2*,                            \
                                                               const int*, const lmkan_b200::InputMap&,           \
                                                               const lmkan_b200::EmitRecords&,                    \
                                                               const lmkan_b200::GridConst*, cudaStream_t);       \
-    template cudaError_t lmkan_b200::launch_gather<OT, double>(const lmkan_b200_layer*,                          \
+    template cudaError_t lmkan_b200::launch_gather<OT, double, DUP>(const lmkan_b200_layer*,                          \
                                                                const lmkan_b200::Plan&, const double*,           \
                                                                const lmkan_b200::OutDests<double>&,              \
                                                                int64_t, const float2*, const int*,               \

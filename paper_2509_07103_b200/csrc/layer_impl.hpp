@@ -15,6 +15,8 @@ struct lmkan_b200_layer {
     double gamma = 0.0;
     int OT = 64, n_ot = 0;
     bool narrow = false;  // n_out <= 4: [pair][node][OT] table, K4 narrow kernel
+    bool dup = false;     // OT = 16 duplicated-node table [ot][pair][node][2][OT] (conflict-free gathers)
+    int ns = 64;          // node stride of the device table in floats (OT, or 2 OT when dup)
     float* table = nullptr;
     size_t table_bytes = 0;
     double* d_inv = nullptr;
@@ -36,8 +38,9 @@ struct Plan {
 };
 
 // Launch the gather kernel variant selected by `pl` for output tile OT
-// (definitions in launch_gather.cuh, instantiated in gather_ot{16,32,64}.cu).
-template <int OT, typename XT>
+// (definitions in launch_gather.cuh, instantiated in gather_ot{16,32,64}.cu and,
+// for duplicated-node OT = 16 tables, gather_ot16d.cu).
+template <int OT, typename XT, bool DUP = false>
 cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                           const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                           const GridConst* gc_next, cudaStream_t st);

@@ -23,6 +23,7 @@
 #include "host_rng.hpp"
 #include "kernels.cuh"
 #include "layer_impl.hpp"
+#include "host_pipeline.hpp"
 
 using namespace lmkan_b200;
 
@@ -120,6 +121,17 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
     return 16;
 }
 
+// Duplicated-node table for an OT = 16 layer (conflict-free 64-B gathers, see
+// fwd_fused_kernel) when its doubled sheet still double-buffers unslabbed in
+// both modes at the tallest row tile, so it never costs sheet reuse (cfg4's
+// G = 16: 37 KB; not G = 28 / 32: 108 / 139 KB). LMKAN_B200_DUP16=0 disables.
+bool choose_dup(int OT, int G, int smem_cap) {
+    if (OT != 16 || !env_int("LMKAN_B200_DUP16", 1)) return false;
+    const int RT = kRTChoices[0] / lane_vectors(OT);
+    return static_cast<int>(fused_smem_layout(G, OT, RT, 2, kModeFused, 1, kWarps, 2 * OT).total) <= smem_cap &&
+           static_cast<int>(fused_smem_layout(G, OT, RT, 2, kModeStaged, 1, kWarps, 2 * OT).total) <= smem_cap;
+}
+
 // Mode: staged (K1 + K2) when several output tiles re-read the same cells (the
 // locate then runs once per (row, pair) instead of once per output tile and
 // the gather kernel's shared-memory port serves only gathers); fused (K3)
@@ -148,16 +160,18 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
     // critical path of the few rows each CTA owns; measured 32 vs 47 us at cfg1)
     const int rt_small = kRTChoices[2] / lane_vectors(L->OT);
     const bool small = ((rows + shape_rt(L->OT, rt_small).R - 1) / shape_rt(L->OT, rt_small).R) * L->n_ot < kNumSMs;
+    const int NSt = L->ns;  // node stride of the table (2 OT for duplicated-node tables)
     const int pref = (L->n_ot >= 3 || small) ? kModeStaged : kModeFused;
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
     for (int mode : modes) {
         if (force_mode >= 0 && mode != force_mode) continue;
         const bool smem_sheet = mode != kModeGlobal;
+        if (L->dup && !smem_sheet) continue;  // duplicated-node tables: shared-memory sheets only
         for (int min_buf : {2, 1}) {
             if (!smem_sheet && min_buf == 2) continue;
             for (int S = 1; S <= (smem_sheet ? kMaxSlabs : 1); ++S) {
                 if (force_s && S != force_s) continue;
-                if (S > 1 && min_buf == 1) continue;
+                if (S > 1 && (min_buf == 1 || L->dup)) continue;
                 for (int A : kRTChoices) {
                     const int RT = A / lane_vectors(L->OT);
                     if (force_rt && RT != force_rt) continue;
@@ -170,12 +184,12 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         if (force_nw) {
                             NW = force_nw;
                         } else {
-                            while (NW > 1 && ((rows + shape_rt(L->OT, RT, NW).R - 1) / shape_rt(L->OT, RT, NW).R) *
+                            while (NW > 1 && ((rows + shape_rt(L->OT, RT, NW, NSt).R - 1) / shape_rt(L->OT, RT, NW, NSt).R) *
                                                      L->n_ot < kNumSMs)
                                 NW >>= 1;
                         }
                     }
-                    const ShapeRT sh = shape_rt(L->OT, RT, NW);
+                    const ShapeRT sh = shape_rt(L->OT, RT, NW, NSt);
                     const int64_t tiles = (rows + sh.R - 1) / sh.R;
                     // a taller row tile reuses each sheet for more rows; take it while the
                     // grid still covers >= 3/4 of the SMs (cfg4: RT 16 with 128 CTAs 0.392 ms
@@ -185,7 +199,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
-                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW);
+                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW, NSt);
                         if (static_cast<int>(s.total) > smem_cap) continue;
                         // Balance: rows per tile Rt <= R so a grid of less than one wave
                         // fills the SMs: cfg4's 128 CTAs of 2048 rows become 147 of 1792
@@ -296,7 +310,10 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
     switch (L->OT) {
         case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
         case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
-        default: e = launch_gather<16, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
+        default:
+            e = L->dup ? launch_gather<16, XT, true>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st)
+                       : launch_gather<16, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st);
+            break;
     }
     if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
@@ -406,7 +423,9 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
         L->OT = no;
     } else {
         L->OT = choose_out_tile(n_out_local, G, max_smem_optin(device));
+        L->dup = choose_dup(L->OT, G, max_smem_optin(device));
     }
+    L->ns = L->dup ? 2 * L->OT : L->OT;
     L->n_ot = (n_out_local + L->OT - 1) / L->OT;
     std::vector<double> pts, inv, t64;
     std::vector<float> t32;
@@ -424,7 +443,7 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     }
     for (int k = 0; k <= kMaxThr; ++k) gc.points[k] = k <= G ? pts[k] : 0.0;
     for (int k = 0; k < kMaxThr; ++k) gc.inv_h[k] = k < G ? 1.0 / (pts[k + 1] - pts[k]) : 0.0;
-    L->table_bytes = static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->OT * sizeof(float);
+    L->table_bytes = static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->ns * sizeof(float);
     cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
     if (e == cudaSuccess)
         e = cudaMemcpy(L->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice);
@@ -454,16 +473,17 @@ template <typename T>
 int relayout_from_device(lmkan_b200_layer* L, const T* P_dev) {
     const size_t total = L->table_bytes / sizeof(float);
     relayout_kernel<T><<<fill_blocks(total), 256>>>(P_dev, L->table, L->pairs, L->nodes, L->n_out_total,
-                                                    L->out_begin, L->n_out, L->OT, L->n_ot);
+                                                    L->out_begin, L->n_out, L->OT, L->ns, L->n_ot);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     return LMKAN_B200_OK;
 }
 
-// Host-path streams (per device, per host thread) for the chunked H2D/compute/D2H pipeline.
-struct HostStreams {
-    cudaStream_t s[2] = {nullptr, nullptr};
-};
+// Host-path pipeline state (streams, events, staging) per device, per host thread.
+HostPipeline& host_pipeline(int device) {
+    static thread_local HostPipeline hp[64];
+    return hp[device & 63];
+}
 
 template <typename XT>
 int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
@@ -472,51 +492,36 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     if (rows == 0) return LMKAN_B200_OK;
     if (!X || !Y) return fail(LMKAN_B200_EINVAL, "lmkan_forward: null X or Y");
     DeviceGuard g(L->device);
-    static thread_local HostStreams hs[64];
-    HostStreams& H = hs[L->device & 63];
-    for (auto& s : H.s)
-        if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    // Chunk so the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernel.
+    HostPipeline& P = host_pipeline(L->device);
+    CK(P.init(L->device));
+    // Chunks flow H2D -> kernels -> D2H on three streams (host_pipeline.hpp).
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
-    // 8 chunks measured best at cfg2 (e2e 19.5 ms vs 20.7 / 22.4 / 23.8 for 4 / 12 / 16;
-    // a tapered first/last chunk measured 20.2): LMKAN_B200_HOST_CHUNKS overrides
-    const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * 148 / std::max(1, L->n_ot);
+    // ~8 chunks of at least one wave of row tiles (cfg2: 8 measured best; fewer
+    // expose more of the first H2D / last D2H, more shrink the grids below a
+    // wave): LMKAN_B200_HOST_CHUNKS overrides
+    const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * kNumSMs / std::max(1, L->n_ot);
     const int64_t nchunks = std::max(1, env_int("LMKAN_B200_HOST_CHUNKS", 8));
     int64_t chunk = std::max<int64_t>({(rows + nchunks - 1) / nchunks, min_chunk, 1});
     chunk = std::min(chunk, rows);
-    const size_t xb = static_cast<size_t>(chunk) * L->n_in * sizeof(XT);
-    const size_t yb = static_cast<size_t>(chunk) * L->n_out * sizeof(XT);
-    XT* dX[2] = {nullptr, nullptr};
-    XT* dY[2] = {nullptr, nullptr};
-    int rc = LMKAN_B200_OK;
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&dX[i]), xb, H.s[i]));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&dY[i]), yb, H.s[i]));
-    }
-    int c = 0;
-    for (int64_t r0 = 0; r0 < rows && rc == LMKAN_B200_OK; r0 += chunk, ++c) {
-        const int i = c & 1;
-        const int64_t n = std::min(chunk, rows - r0);
-        cudaError_t e = cudaMemcpyAsync(dX[i], X + r0 * L->n_in, static_cast<size_t>(n) * L->n_in * sizeof(XT),
-                                        cudaMemcpyHostToDevice, H.s[i]);
-        if (e != cudaSuccess) { rc = cuda_fail(e, "lmkan_forward: H2D"); break; }
-        rc = forward_device<XT>(L, dX[i], dY[i], n, H.s[i]);
-        if (rc) break;
-        e = cudaMemcpyAsync(Y + r0 * L->n_out, dY[i], static_cast<size_t>(n) * L->n_out * sizeof(XT),
-                            cudaMemcpyDeviceToHost, H.s[i]);
-        if (e != cudaSuccess) { rc = cuda_fail(e, "lmkan_forward: D2H"); break; }
-    }
-    for (int i = 0; i < 2; ++i) {
-        cudaFreeAsync(dX[i], H.s[i]);
-        cudaFreeAsync(dY[i], H.s[i]);
-    }
-    for (int i = 0; i < 2; ++i) {
-        cudaError_t e = cudaStreamSynchronize(H.s[i]);
-        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = cuda_fail(e, "lmkan_forward: stream sync");
-    }
-    return rc;
+    CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT), static_cast<size_t>(chunk) * L->n_out * sizeof(XT)));
+    const int64_t chunks = (rows + chunk - 1) / chunk;
+    auto n_of = [&](int64_t c) { return std::min(chunk, rows - c * chunk); };
+    return run_host_pipeline(
+        P, chunks,
+        [&](int64_t c, const void** h, size_t* b) {
+            *h = X + c * chunk * L->n_in;
+            *b = static_cast<size_t>(n_of(c)) * L->n_in * sizeof(XT);
+        },
+        [&](int64_t c, void** h, size_t* b) {
+            *h = Y + c * chunk * L->n_out;
+            *b = static_cast<size_t>(n_of(c)) * L->n_out * sizeof(XT);
+        },
+        [&](int64_t c, void* dX, void* dY, cudaStream_t st) {
+            return forward_device<XT>(L, static_cast<const XT*>(dX), static_cast<XT*>(dY), n_of(c), st);
+        },
+        [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
 }
 
 }  // namespace
@@ -714,7 +719,7 @@ int lmkan_b200_layer_create_random(int n_in, int n_out, int G, double gamma, uin
     DeviceGuard g(device);
     const size_t total = L->table_bytes / sizeof(float);
     fill_random_kernel<<<fill_blocks(total), 256>>>(L->table, L->pairs, L->nodes, L->n_out_total, L->out_begin,
-                                                    L->n_out, L->OT, L->n_ot, seed, static_cast<float>(scale));
+                                                    L->n_out, L->OT, L->ns, L->n_ot, seed, static_cast<float>(scale));
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -733,7 +738,7 @@ int lmkan_b200_layer_read_table(const lmkan_b200_layer* L, int pair_begin, int p
     const size_t count = static_cast<size_t>(L->nodes) * (pair_end - pair_begin) * L->n_out;
     double* tmp = nullptr;
     CK(cudaMalloc(&tmp, count * sizeof(double)));
-    export_kernel<<<fill_blocks(count), 256>>>(L->table, tmp, L->pairs, L->nodes, L->n_out, L->OT, pair_begin,
+    export_kernel<<<fill_blocks(count), 256>>>(L->table, tmp, L->pairs, L->nodes, L->n_out, L->OT, L->ns, pair_begin,
                                                pair_end);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(dst, tmp, count * sizeof(double), cudaMemcpyDeviceToHost);
@@ -806,8 +811,8 @@ int conv_map(const lmkan_b200_layer* L, int N, int H, int W, int C, int k, int s
 }
 }  // namespace
 
-// Synchronous host conv: image chunks alternate over two streams so the H2D of
-// chunk c+1 and the D2H of chunk c-1 overlap the kernels of chunk c.
+// Synchronous host conv: image chunks through the three-stream host pipeline
+// (H2D, kernels and D2H of different chunks overlap; host_pipeline.hpp).
 int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,
                                      int s, float* Y, size_t /*workers*/) {
     InputMap im;
@@ -815,51 +820,37 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
     if (N == 0) return LMKAN_B200_OK;
     if (!img || !Y) return fail(LMKAN_B200_EINVAL, "conv_forward: null image or output");
     DeviceGuard g(L->device);
-    static thread_local HostStreams hs[64];
-    HostStreams& HS = hs[L->device & 63];
-    for (auto& st : HS.s)
-        if (!st) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    HostPipeline& P = host_pipeline(L->device);
+    CK(P.init(L->device));
     const int64_t per_img = static_cast<int64_t>(im.out_h) * im.out_w;
     Plan pl;
     if (!make_plan(L, per_img * N, max_smem_optin(L->device), pl))
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
-    // at least one full wave of CTAs per chunk, else ~8 chunks
-    // chunks of at least one wave of 512-row tiles, so copies overlap kernels (cfg4
-    // e2e: 0.76 ms at 512, 0.81 at 1024, 1.03 as one chunk)
-    // (a full-batch plan's taller tile would otherwise make a single chunk)
+    // chunks of at least one wave of 512-row tiles (a full-batch plan's taller
+    // tile would otherwise make a single chunk), else ~8 chunks
     const int64_t wave_rows = static_cast<int64_t>(env_int("LMKAN_B200_CONV_CHUNK_ROWS", 512)) * kNumSMs /
                               std::max(1, L->n_ot);
     const int64_t min_imgs = (wave_rows + per_img - 1) / per_img;
     const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));
     const size_t in_img = static_cast<size_t>(H) * W * C, out_img = static_cast<size_t>(per_img) * L->n_out;
-    float* dI[2] = {nullptr, nullptr};
-    float* dY[2] = {nullptr, nullptr};
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&dI[i]), sizeof(float) * in_img * chunk, HS.s[i]));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&dY[i]), sizeof(float) * out_img * chunk, HS.s[i]));
-    }
-    int rc = LMKAN_B200_OK;
-    int c = 0;
-    for (int n0 = 0; n0 < N && rc == LMKAN_B200_OK; n0 += chunk, ++c) {
-        const int i = c & 1;
-        const int n = std::min(chunk, N - n0);
-        cudaError_t e = cudaMemcpyAsync(dI[i], img + n0 * in_img, sizeof(float) * in_img * n, cudaMemcpyHostToDevice,
-                                        HS.s[i]);
-        if (e != cudaSuccess) { rc = cuda_fail(e, "conv_forward: H2D"); break; }
-        rc = forward_device<float>(L, dI[i], dY[i], per_img * n, HS.s[i], nullptr, nullptr, im);
-        if (rc) break;
-        e = cudaMemcpyAsync(Y + n0 * out_img, dY[i], sizeof(float) * out_img * n, cudaMemcpyDeviceToHost, HS.s[i]);
-        if (e != cudaSuccess) rc = cuda_fail(e, "conv_forward: D2H");
-    }
-    for (int i = 0; i < 2; ++i) {
-        cudaFreeAsync(dI[i], HS.s[i]);
-        cudaFreeAsync(dY[i], HS.s[i]);
-    }
-    for (int i = 0; i < 2; ++i) {
-        const cudaError_t e = cudaStreamSynchronize(HS.s[i]);
-        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = cuda_fail(e, "conv_forward: stream sync");
-    }
-    return rc;
+    CK(P.reserve(sizeof(float) * in_img * chunk, sizeof(float) * out_img * chunk));
+    const int64_t chunks = (N + chunk - 1) / chunk;
+    auto n_of = [&](int64_t c) { return std::min<int64_t>(chunk, N - c * chunk); };
+    return run_host_pipeline(
+        P, chunks,
+        [&](int64_t c, const void** h, size_t* b) {
+            *h = img + c * chunk * in_img;
+            *b = sizeof(float) * in_img * n_of(c);
+        },
+        [&](int64_t c, void** h, size_t* b) {
+            *h = Y + c * chunk * out_img;
+            *b = sizeof(float) * out_img * n_of(c);
+        },
+        [&](int64_t c, void* dI, void* dY, cudaStream_t st) {
+            return forward_device<float>(L, static_cast<const float*>(dI), static_cast<float*>(dY), per_img * n_of(c),
+                                         st, nullptr, nullptr, im);
+        },
+        [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
 }
 
 int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/lmkan_b200.h"
+#include "host_pipeline.hpp"
 #include "json_mini.hpp"
 #include "layer_impl.hpp"
 
@@ -260,7 +261,8 @@ int format_fail(const InvalidArgument& e) { return api::set_error(LMKAN_B200_EIN
 // [out_begin, out_begin + n_out_local) only (output-sliced layers).
 template <typename T>
 __global__ void relayout_chunk_kernel(const T* __restrict__ src, uint64_t f0, uint64_t n, float* __restrict__ dst,
-                                      int pairs, int nodes, int n_out_total, int out_begin, int n_out_local, int OT) {
+                                      int pairs, int nodes, int n_out_total, int out_begin, int n_out_local, int OT,
+                                      int NS) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t f = f0 + i;
@@ -271,7 +273,10 @@ __global__ void relayout_chunk_kernel(const T* __restrict__ src, uint64_t f0, ui
         const int ql = q - out_begin;
         if (ql < 0 || ql >= n_out_local) continue;
         const int ot = ql / OT, qq = ql - ot * OT;
-        dst[((static_cast<size_t>(ot) * pairs + p) * nodes + node) * OT + qq] = static_cast<float>(src[i]);
+        float* d = dst + ((static_cast<size_t>(ot) * pairs + p) * nodes + node) * NS + qq;
+        const float v = static_cast<float>(src[i]);
+        d[0] = v;
+        if (NS > OT) d[OT] = v;  // duplicated-node table: both copies
     }
 }
 
@@ -329,11 +334,11 @@ int stream_table(const std::string& path, const Lmk1& m, const TensorMeta& t, lm
         if (m.elem == 8)
             relayout_chunk_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dev[b]), f0, n, L->table,
                                                                    L->pairs, L->nodes, L->n_out_total, L->out_begin,
-                                                                   L->n_out, L->OT);
+                                                                   L->n_out, L->OT, L->ns);
         else
             relayout_chunk_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dev[b]), f0, n, L->table,
                                                                   L->pairs, L->nodes, L->n_out_total, L->out_begin,
-                                                                  L->n_out, L->OT);
+                                                                  L->n_out, L->OT, L->ns);
         if ((e = cudaGetLastError()) != cudaSuccess) break;
         if ((e = cudaEventRecord(done[b], st)) != cudaSuccess) break;
     }
@@ -389,23 +394,16 @@ struct lmkan_b200_model {
         cudaGraphExec_t exec;
     };
     std::list<GraphEntry> graphs;  // most recent first, at most kMaxGraphs
-    static constexpr size_t kMaxGraphs = 6;
-    // host path: two streams, device X/Y staging per stream
-    cudaStream_t hst[2] = {nullptr, nullptr};
-    void* hX[2] = {nullptr, nullptr};
-    void* hY[2] = {nullptr, nullptr};
-    size_t hX_bytes = 0, hY_bytes = 0;
+    static constexpr size_t kMaxGraphs = 12;  // host pipeline: 3 slots x (full, tail) chunk + device calls
+    // host path: H2D / chain / D2H pipeline (host_pipeline.hpp)
+    HostPipeline hp;
 
     ~lmkan_b200_model() {
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         for (auto& a : acts)
             for (void* p : a.acts)
                 if (p) cudaFree(p);
-        for (int i = 0; i < 2; ++i) {
-            if (hX[i]) cudaFree(hX[i]);
-            if (hY[i]) cudaFree(hY[i]);
-            if (hst[i]) cudaStreamDestroy(hst[i]);
-        }
+        hp.destroy();
         if (owns)
             for (auto* L : layers) lmkan_b200_layer_destroy(L);
     }
@@ -556,9 +554,9 @@ int infer_device(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows, cudaStre
     return LMKAN_B200_OK;
 }
 
-// Drop-in host path: rows in chunks alternating over two model-owned streams,
-// so the H2D of chunk c+1 and the D2H of chunk c-1 overlap the chain on chunk
-// c; each (chunk shape, stream) replays its own captured graph.
+// Drop-in host path: row chunks through the model's three-stream host pipeline
+// (H2D, chain and D2H of different chunks overlap, host_pipeline.hpp); each
+// chunk shape replays its own captured graph of the chain.
 template <typename XT>
 int infer_host(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows) {
     if (!M || M->layers.empty()) return api::set_error(LMKAN_B200_EINVAL, "model_infer: null or empty model");
@@ -579,49 +577,26 @@ int infer_host(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows) {
         }
     } restore{dev_prev, M->device};
     const int64_t chunk = std::min<int64_t>(rows, std::max<int64_t>((rows + 3) / 4, 65536));
-    const size_t xb = sizeof(XT) * static_cast<size_t>(chunk) * n_in, yb = sizeof(XT) * static_cast<size_t>(chunk) * n_out;
-    for (int i = 0; i < 2; ++i) {
-        cudaError_t e = cudaSuccess;
-        if (!M->hst[i]) e = cudaStreamCreateWithFlags(&M->hst[i], cudaStreamNonBlocking);
-        if (e != cudaSuccess) return api::cuda_error(e, "model_infer: streams");
-    }
-    if (M->hX_bytes < xb || M->hY_bytes < yb) {
-        for (int i = 0; i < 2; ++i) {
-            cudaStreamSynchronize(M->hst[i]);
-            if (M->hX[i]) cudaFree(M->hX[i]);
-            if (M->hY[i]) cudaFree(M->hY[i]);
-            M->hX[i] = M->hY[i] = nullptr;
-        }
-        M->hX_bytes = M->hY_bytes = 0;
-        for (int i = 0; i < 2; ++i) {
-            cudaError_t e = cudaMalloc(&M->hX[i], xb);
-            if (e == cudaSuccess) e = cudaMalloc(&M->hY[i], yb);
-            if (e != cudaSuccess) return api::cuda_error(e, "model_infer: host staging");
-        }
-        M->hX_bytes = xb;
-        M->hY_bytes = yb;
-    }
-    int rc = LMKAN_B200_OK;
-    int c = 0;
-    for (int64_t r0 = 0; r0 < rows && rc == LMKAN_B200_OK; r0 += chunk, ++c) {
-        const int i = c & 1;
-        const int64_t n = std::min(chunk, rows - r0);
-        cudaStream_t st = M->hst[i];
-        cudaError_t e = cudaMemcpyAsync(M->hX[i], X + r0 * n_in, sizeof(XT) * n * n_in, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) {
-            rc = api::cuda_error(e, "model_infer: H2D");
-            break;
-        }
-        rc = infer_device<XT>(M, static_cast<const XT*>(M->hX[i]), static_cast<XT*>(M->hY[i]), n, st);
-        if (rc) break;
-        e = cudaMemcpyAsync(Y + r0 * n_out, M->hY[i], sizeof(XT) * n * n_out, cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) rc = api::cuda_error(e, "model_infer: D2H");
-    }
-    for (int i = 0; i < 2; ++i) {
-        const cudaError_t e = cudaStreamSynchronize(M->hst[i]);
-        if (e != cudaSuccess && rc == LMKAN_B200_OK) rc = api::cuda_error(e, "model_infer: stream sync");
-    }
-    return rc;
+    HostPipeline& P = M->hp;
+    cudaError_t e = P.init(M->device);
+    if (e == cudaSuccess)
+        e = P.reserve(sizeof(XT) * static_cast<size_t>(chunk) * n_in, sizeof(XT) * static_cast<size_t>(chunk) * n_out);
+    if (e != cudaSuccess) return api::cuda_error(e, "model_infer: host staging");
+    auto n_of = [&](int64_t c) { return std::min(chunk, rows - c * chunk); };
+    return run_host_pipeline(
+        P, (rows + chunk - 1) / chunk,
+        [&](int64_t c, const void** h, size_t* b) {
+            *h = X + c * chunk * n_in;
+            *b = sizeof(XT) * static_cast<size_t>(n_of(c)) * n_in;
+        },
+        [&](int64_t c, void** h, size_t* b) {
+            *h = Y + c * chunk * n_out;
+            *b = sizeof(XT) * static_cast<size_t>(n_of(c)) * n_out;
+        },
+        [&](int64_t c, void* dX, void* dY, cudaStream_t st) {
+            return infer_device<XT>(M, static_cast<const XT*>(dX), static_cast<XT*>(dY), n_of(c), st);
+        },
+        [](cudaError_t err, const char* what) { return api::cuda_error(err, what); });
 }
 
 }  // namespace

@@ -8,17 +8,18 @@ namespace lmkan_b200 {
 
 // ------------------------------------------------------- table preparation
 // Reference layout src[node][pair][out_total] (layer.hpp:34-45) -> device layout
-// dst[ot][pair][node][OT] for the output slice [out_begin, out_begin + n_out_local),
-// zero padded to n_ot*OT. One thread per destination element (coalesced on both
-// sides along the output index).
+// dst[ot][pair][node][NS] for the output slice [out_begin, out_begin + n_out_local),
+// zero padded to n_ot*OT; NS = OT, or 2 OT for a duplicated-node table (both
+// copies of a node's OT outputs written). One thread per destination element
+// (coalesced on both sides along the output index).
 template <typename T>
 __global__ void relayout_kernel(const T* __restrict__ src, float* __restrict__ dst, int pairs, int nodes,
-                                int n_out_total, int out_begin, int n_out_local, int OT, int n_ot) {
-    const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * OT;
+                                int n_out_total, int out_begin, int n_out_local, int OT, int NS, int n_ot) {
+    const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * NS;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int qq = static_cast<int>(i % OT);
-        size_t t = i / OT;
+        const int qq = static_cast<int>(i % NS) % OT;  // both copies of a duplicated node
+        size_t t = i / NS;
         const int node = static_cast<int>(t % nodes);
         t /= nodes;
         const int p = static_cast<int>(t % pairs);
@@ -47,13 +48,13 @@ __device__ __forceinline__ float hash_normal(uint64_t seed, uint64_t f) {
 }
 
 static __global__ void fill_random_kernel(float* __restrict__ dst, int pairs, int nodes, int n_out_total,
-                                   int out_begin, int n_out_local, int OT, int n_ot, uint64_t seed,
+                                   int out_begin, int n_out_local, int OT, int NS, int n_ot, uint64_t seed,
                                    float scale) {
-    const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * OT;
+    const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * NS;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int qq = static_cast<int>(i % OT);
-        size_t t = i / OT;
+        const int qq = static_cast<int>(i % NS) % OT;  // both copies of a duplicated node
+        size_t t = i / NS;
         const int node = static_cast<int>(t % nodes);
         t /= nodes;
         const int p = static_cast<int>(t % pairs);
@@ -70,7 +71,7 @@ static __global__ void fill_random_kernel(float* __restrict__ dst, int pairs, in
 
 // Device table -> reference layout (doubles) for pairs [pb, pe), local outputs.
 static __global__ void export_kernel(const float* __restrict__ table, double* __restrict__ dst, int pairs, int nodes,
-                              int n_out_local, int OT, int pb, int pe) {
+                              int n_out_local, int OT, int NS, int pb, int pe) {
     const int np = pe - pb;
     const size_t total = static_cast<size_t>(nodes) * np * n_out_local;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
@@ -80,7 +81,7 @@ static __global__ void export_kernel(const float* __restrict__ table, double* __
         const int pl = static_cast<int>(t % np);
         const int node = static_cast<int>(t / np);
         const int ot = q / OT, qq = q % OT;
-        dst[i] = table[((static_cast<size_t>(ot) * pairs + pb + pl) * nodes + node) * OT + qq];
+        dst[i] = table[((static_cast<size_t>(ot) * pairs + pb + pl) * nodes + node) * NS + qq];
     }
 }
 

@@ -431,3 +431,36 @@ def test_balanced_row_tiles_bitwise(torch, pkg, oracle, monkeypatch, mode):
     assert torch.equal(y_full, y_bal)
     ref = oracle.forward(G, P.astype(np.float64), X[:400].cpu().numpy().astype(np.float64), 1.0)
     assert _mixed(y_bal[:400].cpu().numpy(), ref).max() <= TOL
+
+
+@pytest.mark.parametrize("n_in,n_out,G,force_ot", [(40, 16, 16, None), (30, 13, 8, None), (24, 40, 12, "16")])
+def test_duplicated_node_tables_bitwise(torch, pkg, oracle, monkeypatch, n_in, n_out, G, force_ot):
+    """OT = 16 layers store every node twice (conflict-free gathers): the
+    table reads back as the reference P, and every mode / row tile gives the
+    same bits as the plain table, within the parity bar of the oracle."""
+    if force_ot:
+        monkeypatch.setenv("LMKAN_B200_OT", force_ot)
+    rows = 5000
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in + G)
+    Xd = torch.from_numpy(X).cuda()
+    ref = oracle.forward(G, P.astype(np.float64), X.astype(np.float64), 1.0)
+    layers = {}
+    for dup in ("0", "1"):
+        monkeypatch.setenv("LMKAN_B200_DUP16", dup)
+        layers[dup] = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+        r = pkg.Layer.random(n_in, n_out, G, seed=5)
+        layers["rand" + dup] = r
+    assert layers["1"].out_tile == 16 and layers["1"].table_bytes == 2 * layers["0"].table_bytes
+    np.testing.assert_array_equal(layers["1"].read_table(), P.astype(np.float64))
+    np.testing.assert_array_equal(layers["rand1"].read_table(), layers["rand0"].read_table())
+    base = layers["0"].forward(Xd)
+    for mode in ("fused", "staged"):
+        monkeypatch.setenv("LMKAN_B200_MODE", mode)
+        for rt in ("16", "8", "4"):
+            monkeypatch.setenv("LMKAN_B200_RT", rt)
+            Y = layers["1"].forward(Xd)
+            assert _mixed(Y.cpu().numpy(), ref).max() <= TOL, (mode, rt)
+            assert torch.equal(Y, base), (mode, rt)
+    monkeypatch.delenv("LMKAN_B200_RT")
+    monkeypatch.delenv("LMKAN_B200_MODE")
+    assert torch.equal(layers["rand1"].forward(Xd), layers["rand0"].forward(Xd))
