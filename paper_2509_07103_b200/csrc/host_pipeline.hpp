@@ -17,9 +17,37 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace lmkan_b200 {
+
+// Chunk boundaries over `total` units (rows or images): chunks of `full` units,
+// optionally tapered at both ends (full/4, full/2, full, ..., full, full/2,
+// full/4) so the first H2D and the last kernels + D2H, which nothing overlaps,
+// move less data. Tapering needs at least 2 full chunks' worth of units.
+struct ChunkSchedule {
+    std::vector<int64_t> start;  // start[c] .. start[c + 1]
+    ChunkSchedule(int64_t total, int64_t full, bool taper) {
+        full = full < 1 ? 1 : full;
+        std::vector<int64_t> sizes;
+        if (taper && full >= 4 && total >= 2 * full) {
+            const int64_t edge[2] = {full / 4, full / 2};
+            int64_t mid = total - 2 * (edge[0] + edge[1]);
+            sizes = {edge[0], edge[1]};
+            for (; mid > 0; mid -= full) sizes.push_back(mid < full ? mid : full);
+            sizes.push_back(edge[1]);
+            sizes.push_back(edge[0]);
+        } else {
+            for (int64_t r = total; r > 0; r -= full) sizes.push_back(r < full ? r : full);
+        }
+        start.assign(1, 0);
+        for (int64_t z : sizes) start.push_back(start.back() + z);
+    }
+    int64_t count() const { return static_cast<int64_t>(start.size()) - 1; }
+    int64_t first(int64_t c) const { return start[c]; }
+    int64_t size(int64_t c) const { return start[c + 1] - start[c]; }
+};
 
 struct HostPipeline {
     static constexpr int kSlots = 3;

@@ -506,20 +506,19 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     int64_t chunk = std::max<int64_t>({(rows + nchunks - 1) / nchunks, min_chunk, 1});
     chunk = std::min(chunk, rows);
     CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT), static_cast<size_t>(chunk) * L->n_out * sizeof(XT)));
-    const int64_t chunks = (rows + chunk - 1) / chunk;
-    auto n_of = [&](int64_t c) { return std::min(chunk, rows - c * chunk); };
+    const ChunkSchedule cs(rows, chunk, env_int("LMKAN_B200_HOST_TAPER", 1) != 0);  // cfg2 e2e 3.51e6 -> 3.58e6
     return run_host_pipeline(
-        P, chunks,
+        P, cs.count(),
         [&](int64_t c, const void** h, size_t* b) {
-            *h = X + c * chunk * L->n_in;
-            *b = static_cast<size_t>(n_of(c)) * L->n_in * sizeof(XT);
+            *h = X + cs.first(c) * L->n_in;
+            *b = static_cast<size_t>(cs.size(c)) * L->n_in * sizeof(XT);
         },
         [&](int64_t c, void** h, size_t* b) {
-            *h = Y + c * chunk * L->n_out;
-            *b = static_cast<size_t>(n_of(c)) * L->n_out * sizeof(XT);
+            *h = Y + cs.first(c) * L->n_out;
+            *b = static_cast<size_t>(cs.size(c)) * L->n_out * sizeof(XT);
         },
         [&](int64_t c, void* dX, void* dY, cudaStream_t st) {
-            return forward_device<XT>(L, static_cast<const XT*>(dX), static_cast<XT*>(dY), n_of(c), st);
+            return forward_device<XT>(L, static_cast<const XT*>(dX), static_cast<XT*>(dY), cs.size(c), st);
         },
         [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
 }
@@ -834,21 +833,20 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
     const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));
     const size_t in_img = static_cast<size_t>(H) * W * C, out_img = static_cast<size_t>(per_img) * L->n_out;
     CK(P.reserve(sizeof(float) * in_img * chunk, sizeof(float) * out_img * chunk));
-    const int64_t chunks = (N + chunk - 1) / chunk;
-    auto n_of = [&](int64_t c) { return std::min<int64_t>(chunk, N - c * chunk); };
+    const ChunkSchedule cs(N, chunk, env_int("LMKAN_B200_HOST_TAPER", 0) != 0);  // cfg4 e2e: tapering cost 15%
     return run_host_pipeline(
-        P, chunks,
+        P, cs.count(),
         [&](int64_t c, const void** h, size_t* b) {
-            *h = img + c * chunk * in_img;
-            *b = sizeof(float) * in_img * n_of(c);
+            *h = img + cs.first(c) * in_img;
+            *b = sizeof(float) * in_img * cs.size(c);
         },
         [&](int64_t c, void** h, size_t* b) {
-            *h = Y + c * chunk * out_img;
-            *b = sizeof(float) * out_img * n_of(c);
+            *h = Y + cs.first(c) * out_img;
+            *b = sizeof(float) * out_img * cs.size(c);
         },
         [&](int64_t c, void* dI, void* dY, cudaStream_t st) {
-            return forward_device<float>(L, static_cast<const float*>(dI), static_cast<float*>(dY), per_img * n_of(c),
-                                         st, nullptr, nullptr, im);
+            return forward_device<float>(L, static_cast<const float*>(dI), static_cast<float*>(dY),
+                                         per_img * cs.size(c), st, nullptr, nullptr, im);
         },
         [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
 }
