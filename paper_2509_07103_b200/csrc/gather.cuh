@@ -114,7 +114,7 @@ struct FusedSmem {
     int nrec;
 };
 __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1,
-                                                       int NW = kWarps, int NS = 0) {
+                                                       int NW = kWarps, int NS = 0, int goff = 0) {
     const ShapeRT sh = shape_rt(OT, RT, NW);
     const int H = (G + S - 1) / S;
     const int nb = nbuf > 0 ? nbuf : 1;
@@ -122,7 +122,13 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
     s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
     s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * (NS > 0 ? NS : OT) * 4u;
     s.recw_bytes = sh.R * 8u;  // float2 {alpha, gamma} per row
-    s.reco_bytes = sh.OBLK * 4u;
+    // goff (staged only): node offsets go global -> registers (prefetched a pair
+    // ahead) instead of riding the ring with the records, so the ring holds only
+    // sheets and {alpha, gamma}. The planner uses it only where it buys a taller
+    // row tile (cfg3's G = 28 layer: 2 x 108 KB sheets + 2 x 8 KB records fit
+    // the 1024-row tile, 6.76 -> 5.92 ms per chain step); where the ring fits
+    // either way the shared-memory offsets measured faster (cfg2 17.01 vs 17.15 ms).
+    s.reco_bytes = (mode == kModeStaged && goff) ? 0u : sh.OBLK * 4u;
     uint32_t o = mode == kModeGlobal ? 0u : s.sheet_bytes * nb;
     o = (o + 127u) & ~127u;
     s.off_recw = o;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
 // t_p = ((w00 p00 + w10 p10) + w01 p01) + w11 p11 (fused multiply-adds), the
 // reference's per-pair grouping (layer.hpp:129); then acc * gamma (layer.hpp:131).
 // Deterministic: no data atomics, fixed order, independent of the launch shape.
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW, bool TAIL, bool DUP>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW, bool TAIL, bool DUP, bool GOFF>
 __global__ void __launch_bounds__(NW * 32, 1)
     fwd_fused_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
@@ -273,7 +279,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
     const int H = (G + S - 1) / S;
-    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW, NS);
+    static_assert(!GOFF || MODE == kModeStaged, "GOFF: staged mode only");
+    const FusedSmem L = fused_smem_layout(G, OT, RT, nbuf, MODE, S, NW, NS, GOFF ? 1 : 0);
     float* sheets = reinterpret_cast<float*>(smem);
     float2* rec_w = reinterpret_cast<float2*>(smem + L.off_recw);
     int* rec_o = reinterpret_cast<int*>(smem + L.off_reco);
@@ -345,9 +352,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 const int rs = p % L.nrec;
                 bulk_g2s(reinterpret_cast<char*>(rec_w) + rs * L.recw_bytes,
                          recW + static_cast<size_t>(p) * rows_pad + row0, recw_copy, &full[slot], policy_rec);
-                bulk_g2s(reinterpret_cast<char*>(rec_o) + rs * L.reco_bytes,
-                         recO + (static_cast<size_t>(p) * tiles + tile) * Sh::OBLK, L.reco_bytes, &full[slot],
-                         policy_rec);
+                if (L.reco_bytes)
+                    bulk_g2s(reinterpret_cast<char*>(rec_o) + rs * L.reco_bytes,
+                             recO + (static_cast<size_t>(p) * tiles + tile) * Sh::OBLK, L.reco_bytes, &full[slot],
+                             policy_rec);
             }
         }
     };
@@ -422,7 +430,32 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (pairs > 1) prefetch(1);
         __syncwarp();
     }
-    int offs[RT];
+    // A lane group's RT node offsets (contiguous, 16-B aligned runs of OSTRIDE ints)
+    auto load_offs = [&](const int* ro, int(&o)[RT], bool global) {
+        if constexpr (RT % 4 == 0) {
+#pragma unroll
+            for (int k = 0; k < RT / 4; ++k) {
+                const int4 v = global ? __ldg(reinterpret_cast<const int4*>(ro) + k) : reinterpret_cast<const int4*>(ro)[k];
+                o[4 * k] = v.x;
+                o[4 * k + 1] = v.y;
+                o[4 * k + 2] = v.z;
+                o[4 * k + 3] = v.w;
+            }
+        } else if constexpr (RT == 2) {  // small-batch CTAs at V = 2: OSTRIDE = 6, 8-B aligned runs
+            const int2 v = global ? __ldg(reinterpret_cast<const int2*>(ro)) : *reinterpret_cast<const int2*>(ro);
+            o[0] = v.x;
+            o[1] = v.y;
+        } else {
+            static_assert(RT == 1, "rows per thread: 1, 2 or a multiple of 4");
+            o[0] = global ? __ldg(ro) : ro[0];
+        }
+    };
+    // staged with goff: pair p's offsets come straight from K1's output (recO),
+    // loaded one pair ahead into registers so the latency hides behind a pair's gather
+    const int lane_slot = (warp * Sh::RPW + sub) * Sh::OSTRIDE;
+    auto offs_src = [&](int pp) { return recO + (static_cast<size_t>(pp) * tiles + tile) * Sh::OBLK + lane_slot; };
+    int offs[RT], offs_next[RT];  // offs_next: GOFF only (dead otherwise)
+    if constexpr (GOFF) load_offs(offs_src(0), offs_next, true);
     const float2* rw = rec_w;
     int p = 0, s = 0;
     for (int u = 0; u < units; ++u) {
@@ -434,26 +467,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
         } else {
             sh = tsrc + static_cast<size_t>(p) * sheet_floats + lane_base;
         }
-        if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets to registers (kept across slabs)
+        if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets in registers (kept across slabs)
             const int rs = MODE == kModeStaged ? p % L.nrec : 0;
             rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
-            const int* ro = rec_o + rs * (L.reco_bytes / 4) + (warp * Sh::RPW + sub) * Sh::OSTRIDE;
-            if constexpr (RT % 4 == 0) {
+            if constexpr (GOFF) {
 #pragma unroll
-                for (int k = 0; k < RT / 4; ++k) {
-                    const int4 v = reinterpret_cast<const int4*>(ro)[k];
-                    offs[4 * k] = v.x;
-                    offs[4 * k + 1] = v.y;
-                    offs[4 * k + 2] = v.z;
-                    offs[4 * k + 3] = v.w;
-                }
-            } else if constexpr (RT == 2) {  // small-batch CTAs at V = 2: OSTRIDE = 6, 8-B aligned runs
-                const int2 v = *reinterpret_cast<const int2*>(ro);
-                offs[0] = v.x;
-                offs[1] = v.y;
+                for (int j = 0; j < RT; ++j) offs[j] = offs_next[j];
+                if (p + 1 < pairs) load_offs(offs_src(p + 1), offs_next, true);
             } else {
-                static_assert(RT == 1, "rows per thread: 1, 2 or a multiple of 4");
-                offs[0] = ro[0];
+                load_offs(rec_o + rs * (L.reco_bytes / 4) + lane_slot, offs, false);
             }
         }
         if (!TAIL || warp_live) {  // TAIL: shortened row tiles, some warps hold no rows

@@ -6,11 +6,12 @@
 
 namespace lmkan_b200 {
 
-template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps, bool TAIL = false, bool DUP = false>
+template <int OT, int RT, typename XT, int MODE, bool SLAB, int NW = kWarps, bool TAIL = false, bool DUP = false,
+          bool GOFF = false>
 cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                            const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
-    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL, DUP>;
+    auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL, DUP, GOFF>;
     static int configured[64] = {0};  // per device: dynamic-smem opt-in done
     const int dev = L->device & 63;
     if (!configured[dev]) {
@@ -32,6 +33,15 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
     // rows per thread: the planner's {16, 8, 4} float4 accumulators per thread / V
     constexpr int V = lane_vectors(OT);
     constexpr int RT0 = 16 / V, RT1 = 8 / V, RT2 = 4 / V;
+    if constexpr (MODE == kModeStaged && !SLAB && !DUP) {  // offsets from global: the tallest tile only (planner)
+        if (pl.goff) {
+            if (pl.row_tile < pl.sh.R)
+                return launch_fused_t<OT, RT0, XT, MODE, false, kWarps, true, false, true>(L, pl, X, Y, rows, recW,
+                                                                                           recO, im, emit, gc_next, st);
+            return launch_fused_t<OT, RT0, XT, MODE, false, kWarps, false, false, true>(L, pl, X, Y, rows, recW, recO,
+                                                                                        im, emit, gc_next, st);
+        }
+    }
     if constexpr (!SLAB) {  // small batches: fewer warps per CTA (RT2) so the grid still spans the GPU
         switch (pl.sh.NW) {
             case 8: return launch_fused_t<OT, RT2, XT, MODE, false, 8, false, DUP>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);

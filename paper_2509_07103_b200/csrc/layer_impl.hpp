@@ -35,6 +35,7 @@ struct Plan {
     int64_t row_tiles, rows_pad;
     int launches;
     int64_t row_tile;  // rows per CTA tile, <= sh.R (smaller to balance the grid over the SMs)
+    int goff = 0;      // staged: node offsets read from global into registers (fwd_fused_kernel)
 };
 
 // Launch the gather kernel variant selected by `pl` for output tile OT

@@ -112,7 +112,9 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
             for (int OT : {64, 32, 16}) {
                 if (OT > 16 && OT / 2 >= n_out) continue;
                 for (int A : kRTChoices) {
-                    const FusedSmem s = fused_smem_layout(G, OT, A / lane_vectors(OT), want_buf, kModeStaged, S);
+                    // (global offsets: the tallest tile, unslabbed, only; see make_plan)
+                    const FusedSmem s = fused_smem_layout(G, OT, A / lane_vectors(OT), want_buf, kModeStaged, S,
+                                                          kWarps, 0, A == kRTChoices[0] && S == 1 ? 1 : 0);
                     if (static_cast<int>(s.total) <= smem_cap) return OT;
                 }
             }
@@ -199,7 +201,14 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
                         if (smem_sheet && nbuf > units && nbuf > 1) continue;
-                        const FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW, NSt);
+                        // staged: offsets through the ring, else (when only that fits) from global
+                        int goff = 0;
+                        FusedSmem s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW, NSt);
+                        if (static_cast<int>(s.total) > smem_cap && mode == kModeStaged && A == kRTChoices[0] &&
+                            S == 1 && NW == kWarps && !L->dup && env_int("LMKAN_B200_GOFF", 1)) {
+                            goff = 1;
+                            s = fused_smem_layout(L->G, L->OT, RT, nbuf, mode, S, NW, NSt, 1);
+                        }
                         if (static_cast<int>(s.total) > smem_cap) continue;
                         // Balance: rows per tile Rt <= R so a grid of less than one wave
                         // fills the SMs: cfg4's 128 CTAs of 2048 rows become 147 of 1792
@@ -221,7 +230,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                             }
                         }
                         out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, nt, nt * Rt,
-                                   mode == kModeStaged ? 2 : 1, Rt};
+                                   mode == kModeStaged ? 2 : 1, Rt, goff};
                         return true;
                     }
                 }

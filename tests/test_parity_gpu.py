@@ -464,3 +464,25 @@ def test_duplicated_node_tables_bitwise(torch, pkg, oracle, monkeypatch, n_in, n
     monkeypatch.delenv("LMKAN_B200_RT")
     monkeypatch.delenv("LMKAN_B200_MODE")
     assert torch.equal(layers["rand1"].forward(Xd), layers["rand0"].forward(Xd))
+
+
+@pytest.mark.parametrize("rows", [30000, 150000])  # balanced (shortened) tall tiles / full tiles
+def test_global_offsets_tall_tile_bitwise(torch, pkg, oracle, monkeypatch, rows):
+    """Staged layers whose ring only fits the taller row tile with the node
+    offsets read from global memory (cfg3's 128->128 G=28 layer: 1024 rows per
+    CTA instead of 512) give the same bits as the shorter tile, within the
+    parity bar."""
+    n_in, n_out, G = 128, 128, 28
+    P, X = _inputs(torch, n_in, n_out, G, rows, seed=28)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    Xd = torch.from_numpy(X).cuda()
+    outs = {}
+    for goff in ("1", "0"):
+        monkeypatch.setenv("LMKAN_B200_GOFF", goff)
+        outs[goff] = (layer.plan(rows), layer.forward(Xd))
+    assert outs["1"][0]["rows_per_thread"] == 2 * outs["0"][0]["rows_per_thread"], (outs["1"][0], outs["0"][0])
+    assert outs["1"][0]["rows_per_cta"] > 512, outs["1"][0]
+    assert torch.equal(outs["1"][1], outs["0"][1])
+    sub = slice(0, 2000)
+    ref = oracle.forward(G, P.astype(np.float64), X[sub].astype(np.float64), 1.0)
+    assert _mixed(outs["1"][1][sub].cpu().numpy(), ref).max() <= TOL
