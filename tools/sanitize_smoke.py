@@ -1,6 +1,7 @@
 """Small forwards through every kernel family, for compute-sanitizer runs
 (memcheck / racecheck / synccheck): staged, fused, global, slabbed, narrow,
-small-batch warps, conv, model chain, backward, multi-destination epilogue."""
+small-batch warps, duplicated-node tables, global node offsets, conv, model
+chain, backward, multi-destination epilogue."""
 import os
 import sys
 
@@ -29,6 +30,9 @@ run({"LMKAN_B200_MODE": "staged", "LMKAN_B200_SLABS": "2"}, 40, 72, 28, 700)
 run({"LMKAN_B200_MODE": "global"}, 40, 72, 12, 300)
 run({"LMKAN_B200_NW": "2", "LMKAN_B200_RT": "4"}, 64, 64, 8, 100)
 run({}, 128, 1, 28, 3000)
+run({}, 40, 16, 16, 3000)  # OT = 16 duplicated-node table (fused)
+run({"LMKAN_B200_MODE": "staged"}, 40, 16, 16, 3000)  # DUP, staged
+run({}, 128, 128, 28, 40000)  # staged 1024-row tile with node offsets from global (GOFF)
 run({}, 12, 128, 28, 2000)
 lay = pkg.Layer.random(144, 16, 16, seed=2)
 img = torch.randn((3, 10, 10, 16), device="cuda")
