@@ -486,3 +486,20 @@ def test_global_offsets_tall_tile_bitwise(torch, pkg, oracle, monkeypatch, rows)
     sub = slice(0, 2000)
     ref = oracle.forward(G, P.astype(np.float64), X[sub].astype(np.float64), 1.0)
     assert _mixed(outs["1"][1][sub].cpu().numpy(), ref).max() <= TOL
+
+
+def test_empty_batches(torch, pkg):
+    """Zero rows (or zero images) are a no-op on every entry, like the
+    reference's lmkan_forward on an empty Matrix (layer.hpp:111-118)."""
+    layer = pkg.Layer.random(16, 8, 6, seed=1)
+    Y = layer.forward(torch.empty((0, 16), device="cuda"))
+    assert tuple(Y.shape) == (0, 8)
+    for dt in (np.float32, np.float64):
+        assert layer.forward_host(np.empty((0, 16), dt)).shape == (0, 8)
+    assert pkg.lmkan_forward(pkg.init_layer(16, 8, 6, seed=1), np.empty((0, 16))).shape == (0, 8)
+    conv = pkg.Layer.random(2 * 2 * 4, 8, 5, seed=2)
+    assert tuple(conv.conv_forward(torch.zeros((0, 6, 6, 4), device="cuda"), 2, 1).shape) == (0, 5, 5, 8)
+    assert conv.conv_forward_host(np.zeros((0, 6, 6, 4), np.float32), 2, 1).shape == (0, 5, 5, 8)
+    m = pkg.Model.from_layers([pkg.Layer.random(12, 32, 8, seed=3), pkg.Layer.random(32, 2, 8, seed=4)])
+    assert m.infer_host(np.empty((0, 12), np.float32)).shape == (0, 2)
+    assert tuple(m.infer(torch.empty((0, 12), device="cuda")).shape) == (0, 2)
