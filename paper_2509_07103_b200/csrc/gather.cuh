@@ -188,12 +188,20 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
         if (tid < 32) coff[tid] = in_coloff(im, 2 * p0 + tid);
         __syncthreads();
         XT v[8];  // all 8 loads of this thread in flight before any store
+        if (!im.conv) {  // dense X: rows n_in apart, no per-element address lookup
+            const int rr0 = tid >> 5, c = tid & 31, col = 2 * p0 + c;
+            const XT* xp = X + (r0 + rr0 + im.row_offset) * n_in + col;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int i = tid + 256 * t;
-            const int rr = i >> 5, c = i & 31;
-            const int col = 2 * p0 + c;
-            v[t] = (r0 + rr < rows && col < n_in) ? __ldg(X + rbase[rr] + coff[c]) : XT(0);
+            for (int t = 0; t < 8; ++t)
+                v[t] = (r0 + rr0 + 8 * t < rows && col < n_in) ? __ldg(xp + static_cast<int64_t>(8 * t) * n_in) : XT(0);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int i = tid + 256 * t;
+                const int rr = i >> 5, c = i & 31;
+                const int col = 2 * p0 + c;
+                v[t] = (r0 + rr < rows && col < n_in) ? __ldg(X + rbase[rr] + coff[c]) : XT(0);
+            }
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
