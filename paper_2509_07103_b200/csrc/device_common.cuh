@@ -133,6 +133,12 @@ __device__ __forceinline__ float2 lds64_if(const void* p, bool pred) {
         : "memory");
     return v;
 }
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p 32-byte aligned.
+__device__ __forceinline__ void ldg_v8(const float* p, float (&o)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+                 : "l"(p));
+}
 __device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned* p, unsigned v) {
     unsigned old;
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_addr(p)), "r"(v) : "memory");

@@ -237,6 +237,64 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     }
 }
 
+// K1 (staged path), register-direct variant: one thread per (row, group of 4
+// pairs), no shared-memory staging and no barriers. The group's 8 inputs are
+// contiguous in X (dense rows; conv rows when C % 8 == 0), so a 32-byte load
+// fetches them; consecutive threads take consecutive rows, so the {alpha,
+// gamma} stores of a pair are coalesced. Same records, same order as
+// records_kernel (locate_ag, offset_slot); rows in [rows, rows_pad) get zeros.
+template <typename XT, bool SHORT_TILES>
+__global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
+                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
+                                                       int H, float2* __restrict__ W, int* __restrict__ O,
+                                                       const InputMap im, int64_t Rt, int vec) {
+    __shared__ XT thr[kMaxThr];
+    __shared__ double pts[kMaxThr + 1];
+    __shared__ double invh[kMaxThr];
+    const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
+    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
+    for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
+    __syncthreads();
+    const int p0 = blockIdx.y * 4;
+    const int np = pairs - p0 < 4 ? pairs - p0 : 4;
+    const int64_t tiles = SHORT_TILES ? rows_pad / Rt : rows_pad >> sh.lgR;
+    const int c0 = in_coloff(im, 2 * p0);
+    const size_t wstep = static_cast<size_t>(rows_pad), ostep = static_cast<size_t>(tiles) * sh.OBLK;
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * 256 + tid; g < rows_pad; g += static_cast<int64_t>(gridDim.x) * 256) {
+        XT x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = XT(0);
+        if (g < rows) {
+            const XT* xr = X + in_rowbase(im, g, n_in);
+            if (sizeof(XT) == 4 && vec && np == 4) {  // 8 contiguous, 32-byte aligned inputs
+                float u[8];
+                ldg_v8(reinterpret_cast<const float*>(xr + c0), u);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x[k] = static_cast<XT>(u[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k < 2 * np) x[k] = __ldg(xr + in_coloff(im, 2 * p0 + k));
+            }
+        }
+        const int64_t tile = SHORT_TILES ? g / Rt : g >> sh.lgR;
+        const int slot = offset_slot(sh, static_cast<int>(g - tile * Rt));
+        float2* wp = W + static_cast<size_t>(p0) * wstep + g;
+        int* op = O + (static_cast<size_t>(p0) * tiles + tile) * sh.OBLK + slot;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k < np) {
+                float2 ag = make_float2(0.f, 0.f);
+                int packed = 0;
+                if (g < rows) packed = locate_ag<XT>(x[2 * k], x[2 * k + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag);
+                wp[k * wstep] = ag;
+                op[k * ostep] = packed;
+            }
+        }
+    }
+}
+
 // K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
 // Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
 // [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of

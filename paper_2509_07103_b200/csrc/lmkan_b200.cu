@@ -295,16 +295,32 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
             cudaFreeAsync(recW, st);
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
-        const int64_t py = (L->pairs + 15) / 16;
-        const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
-        dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         const int H = (L->G + pl.S - 1) / pl.S;
-        if (pl.row_tile < pl.sh.R)
-            records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                         im, pl.row_tile);
-        else
-            records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                          im, pl.row_tile);
+        if (env_int("LMKAN_B200_K1", 4) == 4) {  // register-direct K1 (records4_kernel)
+            const int64_t py = (L->pairs + 3) / 4;
+            const int64_t gx = std::min<int64_t>((pl.rows_pad + 255) / 256,
+                                                 std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
+            dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
+            // 32-byte group loads: 8 contiguous inputs at 32-byte aligned offsets
+            const bool vec = (reinterpret_cast<uintptr_t>(X) & 31) == 0 &&
+                             (im.conv ? (im.C % 8 == 0) : (L->n_in % 8 == 0));
+            if (pl.row_tile < pl.sh.R)
+                records4_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
+                                                              recO, im, pl.row_tile, vec ? 1 : 0);
+            else
+                records4_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
+                                                               recO, im, pl.row_tile, vec ? 1 : 0);
+        } else {
+            const int64_t py = (L->pairs + 15) / 16;
+            const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
+            dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
+            if (pl.row_tile < pl.sh.R)
+                records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                             im, pl.row_tile);
+            else
+                records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                              im, pl.row_tile);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(recW, st);

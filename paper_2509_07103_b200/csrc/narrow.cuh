@@ -57,6 +57,11 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
     mbar_wait(bar, 0);
     const int rs1 = (G + 1) * NO;
     const bool vec4 = sizeof(XT) == 4 && !im.conv && (n_in & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    // 256-bit loads (LDG.E.ENL2.256): a lane's 4 pairs in one instruction. The
+    // lanes of a warp read 32 different rows, so every load instruction costs a
+    // wavefront per row; one 32-B load instead of two 16-B ones halves them
+    // (the kernel is L1-bound on these uncoalesced row reads).
+    const bool vec8 = vec4 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;
     for (int64_t r = static_cast<int64_t>(blockIdx.x) * kNarrowThreads + tid; r < rows;
          r += static_cast<int64_t>(gridDim.x) * kNarrowThreads) {
         float acc[NO];
@@ -73,7 +78,16 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
                 acc[q] += fmaf(w.w, b[rs1 + NO + q], fmaf(w.z, b[NO + q], fmaf(w.y, b[rs1 + q], w.x * b[q])));
         };
         int p = 0;
-        if (vec4) {
+        if (vec8) {
+            for (; p + 4 <= pairs; p += 4) {  // one 32-byte sector of the row = 4 pairs, one load
+                float u[8];
+                ldg_v8(reinterpret_cast<const float*>(xr) + 2 * p, u);
+                one_pair(p, u[0], u[1]);
+                one_pair(p + 1, u[2], u[3]);
+                one_pair(p + 2, u[4], u[5]);
+                one_pair(p + 3, u[6], u[7]);
+            }
+        } else if (vec4) {
             for (; p + 4 <= pairs; p += 4) {  // one 32-byte sector of the row = 4 pairs
                 const float4 u = __ldg(reinterpret_cast<const float4*>(xr + 2 * p));
                 const float4 v = __ldg(reinterpret_cast<const float4*>(xr + 2 * p + 4));
