@@ -85,7 +85,11 @@ __global__ void __launch_bounds__(256) locate_kernel(const XT* __restrict__ X, i
 template <typename XT>
 __device__ __forceinline__ int cell_index_fast(XT x, const XT* thr, int G, int L) {
     const float xf = static_cast<float>(x);
-    const float e = __expf(-fabsf(xf));
+    // e = exp(-|x|) as one MUFU.EX2 (ftz: no range fix-up; the estimate is
+    // verified against the exact thresholds below, so its accuracy only decides
+    // how often the fallback search runs)
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(xf) * -1.4426950408889634f));
     const float s = xf > 0.f ? 1.f - 0.5f * e : 0.5f * e;
     int i = static_cast<int>(s * static_cast<float>(G));
     i = i < 0 ? 0 : (i > G - 1 ? G - 1 : i);
@@ -124,6 +128,7 @@ __device__ __forceinline__ int locate_ag(XT x1, XT x2, const XT* thr, const doub
     const int i2 = cell_index_fast<XT>(x2, thr, G, L);
     ag.x = __double2float_rn(__dmul_rn(__dsub_rn(pts[i1 + 1], static_cast<double>(x1)), invh[i1]));
     ag.y = __double2float_rn(__dmul_rn(__dsub_rn(pts[i2 + 1], static_cast<double>(x2)), invh[i2]));
+    if (H >= G) return (i1 * (G + 1) + i2) * OT;  // unslabbed sheet (the common case)
     const int s = (i1 >= H) + (i1 >= 2 * H) + (i1 >= 3 * H);  // slab (S <= 4), no integer division
     return (s << kSlabShift) | (((i1 - s * H) * (G + 1) + i2) * OT);
 }
