@@ -120,6 +120,23 @@ template <class Src, class Dst, class Compute, class Fail>
 int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute compute, Fail cuda_fail) {
     constexpr int S = HostPipeline::kSlots;
     int rc = 0;
+    if (chunks == 1) {  // nothing to overlap: one stream, no cross-stream events (small batches)
+        const void* hs = nullptr;
+        void* hd = nullptr;
+        size_t xb = 0, yb = 0;
+        src(0, &hs, &xb);
+        dst(0, &hd, &yb);
+        cudaStream_t st = P.comp[0];
+        cudaError_t e = cudaMemcpyAsync(P.dX[0], hs, xb, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "host pipeline: H2D");
+        if ((rc = compute(0, P.dX[0], P.dY[0], st)) != 0) {
+            cudaStreamSynchronize(st);
+            return rc;
+        }
+        e = cudaMemcpyAsync(hd, P.dY[0], yb, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? 0 : cuda_fail(e, "host pipeline: D2H");
+    }
     for (int64_t c = 0; c < chunks && rc == 0; ++c) {
         const int b = static_cast<int>(c % S);
         const void* hs = nullptr;

@@ -503,3 +503,21 @@ def test_empty_batches(torch, pkg):
     m = pkg.Model.from_layers([pkg.Layer.random(12, 32, 8, seed=3), pkg.Layer.random(32, 2, 8, seed=4)])
     assert m.infer_host(np.empty((0, 12), np.float32)).shape == (0, 2)
     assert tuple(m.infer(torch.empty((0, 12), device="cuda")).shape) == (0, 2)
+
+
+@pytest.mark.parametrize("taper", ["0", "1"])
+def test_host_pipeline_multichunk_bitwise(torch, pkg, monkeypatch, taper):
+    """The host entry points stream rows through the three-stage pipeline in
+    several (optionally tapered) chunks; results equal the single device launch
+    bitwise, for the layer, the model chain and odd chunk remainders."""
+    monkeypatch.setenv("LMKAN_B200_HOST_TAPER", taper)
+    monkeypatch.setenv("LMKAN_B200_HOST_CHUNKS", "7")
+    layer = pkg.Layer.random(256, 96, 10, seed=21)
+    rows = 123457
+    X = torch.randn((rows, 256), device="cuda")
+    Yd = layer.forward(X).cpu().numpy()
+    Xh = X.cpu().numpy()
+    assert np.array_equal(layer.forward_host(Xh), Yd)
+    m = pkg.Model.from_layers([pkg.Layer.random(12, 64, 8, seed=3), pkg.Layer.random(64, 2, 8, seed=4)])
+    Xm = torch.randn((300001, 12), device="cuda")
+    assert np.array_equal(m.infer_host(Xm.cpu().numpy()), m.infer(Xm).cpu().numpy())
