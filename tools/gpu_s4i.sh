@@ -1,0 +1,3 @@
+set -x
+O=gpurun_out/s4i; mkdir -p $O
+VARS="old f32" CFGS="4 3" timeout 900 bash tools/ab_run.sh > $O/ab.txt 2>&1; cut -c1-60 $O/ab.txt
