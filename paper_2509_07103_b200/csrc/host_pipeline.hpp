@@ -102,12 +102,17 @@ struct HostPipeline {
     void destroy() {
         release();
         for (int i = 0; i < kSlots; ++i)
-            for (cudaEvent_t ev : {h2d[i], kdone[i], d2h[i]})
-                if (ev) cudaEventDestroy(ev);
+            for (cudaEvent_t* ev : {&h2d[i], &kdone[i], &d2h[i]}) {
+                if (*ev) cudaEventDestroy(*ev);
+                *ev = nullptr;
+            }
         for (cudaStream_t s : {in, comp[0], comp[1], out})
             if (s) cudaStreamDestroy(s);
         in = out = comp[0] = comp[1] = nullptr;
     }
+    // per-thread pipelines (host entry points) go away with their thread;
+    // errors after the runtime has shut down (process exit) are ignored
+    ~HostPipeline() { destroy(); }
 };
 
 // Runs `chunks` chunks through the pipeline. For chunk c:
