@@ -521,3 +521,25 @@ def test_host_pipeline_multichunk_bitwise(torch, pkg, monkeypatch, taper):
     m = pkg.Model.from_layers([pkg.Layer.random(12, 64, 8, seed=3), pkg.Layer.random(64, 2, 8, seed=4)])
     Xm = torch.randn((300001, 12), device="cuda")
     assert np.array_equal(m.infer_host(Xm.cpu().numpy()), m.infer(Xm).cpu().numpy())
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows,mode", [(64, 64, 8, 60000, "staged"), (64, 32, 8, 120000, "staged"),
+                                                     (64, 64, 8, 60000, "fused"), (48, 32, 12, 120000, "fused")])
+def test_balanced_tiles_lane_runs_bitwise(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows, mode):
+    """Shortened (balanced) row tiles with several float4 runs per lane
+    (OT = 64: V = 4, OT = 32: V = 2, bank-half interleave) give the same bits
+    as the full tiles and meet the parity bar."""
+    rng = np.random.default_rng(rows + n_out)
+    P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    X = torch.randn((rows, n_in), device="cuda")
+    monkeypatch.setenv("LMKAN_B200_MODE", mode)
+    outs = []
+    for bal in ("0", "1"):
+        monkeypatch.setenv("LMKAN_B200_BALANCE", bal)
+        outs.append((layer.plan(rows), layer.forward(X)))
+    (p_full, y_full), (p_bal, y_bal) = outs
+    assert p_bal["lane_vectors"] == n_out // 16 and p_bal["rows_per_cta"] < p_full["rows_per_cta"], (p_full, p_bal)
+    assert torch.equal(y_full, y_bal)
+    ref = oracle.forward(G, P.astype(np.float64), X[:300].double().cpu().numpy(), 1.0)
+    assert _mixed(y_bal[:300].cpu().numpy(), ref).max() <= TOL
