@@ -238,6 +238,24 @@ def test_f64_device_path(torch, pkg, oracle):
     assert _mixed(Y, ref).max() <= TOL
 
 
+@pytest.mark.parametrize("n_in,n_out,G,rows", [(128, 128, 28, 30000),   # staged, 1024-row tiles, GOFF
+                                               (144, 16, 16, 20000),     # fused, DUP table
+                                               (256, 64, 16, 20000)])    # staged, V = 4 lane runs
+def test_f64_io_matches_f32_io_bitwise(torch, pkg, oracle, n_in, n_out, G, rows):
+    """fp64 I/O runs the same fp32 gathers: on fp32-representable inputs the
+    cells (fp64 vs fp32 thresholds) and {alpha, gamma} agree, so Y is the fp32
+    path's Y widened, bit for bit, in every kernel family; and it meets the
+    parity bar."""
+    layer = pkg.Layer.random(n_in, n_out, G, seed=n_in + G)
+    X32 = torch.randn((rows, n_in), device="cuda") * 1.3
+    Y32 = layer.forward(X32)
+    Y64 = layer.forward(X32.double())
+    assert Y64.dtype == torch.float64
+    assert torch.equal(Y64, Y32.double())
+    ref = oracle.forward(G, layer.read_table(), X32[:300].double().cpu().numpy(), 1.0)
+    assert _mixed(Y64[:300].cpu().numpy(), ref).max() <= TOL
+
+
 VARIANTS = [("fused", "1", "16"), ("fused", "2", "8"), ("fused", "3", "4"), ("staged", "1", "16"),
             ("staged", "2", "16"), ("staged", "3", "8"), ("staged", "4", "4"), ("global", "1", "4"),
             # OT = 64 runs two float4 runs per lane: rows per thread 8 / 4 / 2
