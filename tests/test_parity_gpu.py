@@ -561,3 +561,21 @@ def test_balanced_tiles_lane_runs_bitwise(torch, pkg, oracle, monkeypatch, n_in,
     assert torch.equal(y_full, y_bal)
     ref = oracle.forward(G, P.astype(np.float64), X[:300].double().cpu().numpy(), 1.0)
     assert _mixed(y_bal[:300].cpu().numpy(), ref).max() <= TOL
+
+
+def test_output_slices_across_table_layouts_bitwise(torch, pkg):
+    """Output slices of one layer land on different table layouts (64-wide
+    tiles with 4 float4 runs per lane, 32-wide with 2, 16-wide duplicated-node
+    tables); every slice equals the matching columns of the full layer, bit for
+    bit, and its table reads back exactly."""
+    n_in, n_out, G, rows = 40, 112, 12, 6000
+    rng = np.random.default_rng(40)
+    P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
+    Pd = torch.from_numpy(P).cuda()
+    X = torch.randn((rows, n_in), device="cuda")
+    full = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0)
+    Y = full.forward(X)
+    for ob, oe in [(0, 16), (16, 48), (48, 112), (100, 112)]:
+        sl = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0, out_range=(ob, oe))
+        assert torch.equal(sl.forward(X), Y[:, ob:oe]), (ob, oe, sl.out_tile)
+        np.testing.assert_array_equal(sl.read_table(), P[..., ob:oe].astype(np.float64))
