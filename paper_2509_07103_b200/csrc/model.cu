@@ -21,6 +21,7 @@
 // (rows, X, Y, stream) shape has been seen.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <memory>
@@ -576,7 +577,10 @@ int infer_host(lmkan_b200_model* M, const XT* X, XT* Y, int64_t rows) {
             if (d != cur) cudaSetDevice(d);
         }
     } restore{dev_prev, M->device};
-    const int64_t chunk = std::min<int64_t>(rows, std::max<int64_t>((rows + 3) / 4, 65536));
+    // ~4 chunks of at least 65536 rows (LMKAN_B200_MODEL_CHUNKS overrides the count)
+    const char* ce = std::getenv("LMKAN_B200_MODEL_CHUNKS");
+    const int64_t nch = std::max<int64_t>(1, ce ? std::atoi(ce) : 4);
+    const int64_t chunk = std::min<int64_t>(rows, std::max<int64_t>((rows + nch - 1) / nch, 65536));
     HostPipeline& P = M->hp;
     cudaError_t e = P.init(M->device);
     if (e == cudaSuccess)
