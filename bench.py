@@ -157,6 +157,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(win)}
 
 
+def config_dict(cfg: dict, ws: int, rank: int, shards: int, gather: str) -> dict:
+    """The workload description, identical in both arms (b200 and reference)."""
+    B = cfg["batch"]
+    out_sharded = bool(cfg.get("out_sharded"))
+    if out_sharded:
+        par = (f"output-sharded over {shards} (this run: {ws} process(es); shard {rank % shards}"
+               + ((", all-gather of Y columns fused into the epilogue (NVLink peer stores)" if gather == "fused"
+                   else ", NCCL all-gather of Y columns") if ws > 1 else
+                  ", no all-gather: single-rank shard measurement") + ")")
+    else:
+        par = f"dp{ws} (batch rows, no collective)"
+    return {"workload": cfg["name"], "layers": cfg["layers"], "G": cfg["G"], "batch_per_gpu": B,
+            "global_batch": B if out_sharded else ws * B, "parallelism": par}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -165,11 +180,14 @@ def dist_env():
 
 
 # ------------------------------------------------------------------- CPU reference
-def cpu_reference(cfg: dict, tables, budget_s: float = 12.0):
+def cpu_reference(cfg: dict, tables, step_s: float = 0.5, steps: int = 0, warmup: int = 0, budget_s: float = 12.0):
     """The reference's own lmkan_forward (oracle/_ref/liblmkan_ref.so compiled
-    from /root/reference) on this host, all cores (LMKAN_THREADS = nproc),
-    on a bounded row sample of the workload; 10/20-style protocol shortened
-    to fit budget_s. Returns (samples/s median, cores, sample description, kind)."""
+    from /root/reference) on this host, all cores (LMKAN_THREADS = nproc).
+    A CPU step = one pass of the layer chain over a bounded row sample of the
+    workload, sized (by doubling from 64 rows) to take about step_s seconds.
+    steps > 0: exactly `warmup` untimed + `steps` timed steps (the reference
+    arm); else as many timed steps as fit budget_s (3..20, the cpu_baseline
+    leg). Returns dict(rows, step_times, cores, kind)."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
@@ -214,22 +232,21 @@ def cpu_reference(cfg: dict, tables, budget_s: float = 12.0):
         return spent
 
     rows = 64
-    while True:
+    while True:  # calibrate the sample: double until a pass takes >= step_s / 2
         dt = run_chain(rows)
-        if dt > 0.3 or rows >= cfg["batch"]:
+        if dt >= step_s / 2 or rows >= cfg["batch"]:
             break
-        rows = min(cfg["batch"], rows * 4)
-    per_run = max(dt, 1e-6)
-    reps = int(max(3, min(20, budget_s / per_run)))
-    warm = 1 if per_run > 1.0 else 2
-    for _ in range(warm):
+        rows = min(cfg["batch"], rows * 2)
+    if steps <= 0:
+        steps = int(max(3, min(20, budget_s / max(dt, 1e-6))))
+        warmup = 1 if dt > 1.0 else 2
+    for _ in range(warmup):
         run_chain(rows)
-    ts = [run_chain(rows) for _ in range(reps)]
+    ts = [run_chain(rows) for _ in range(steps)]
     for lay in layers:
         if ref is not None:
             lay.close()
-    med = statistics.median(ts)
-    return rows / med, cores, f"{rows} rows x {reps} timed runs (median, {warm} warm-up) of the {cfg['name']} workload", kind
+    return dict(rows=rows, step_times=ts, cores=cores, kind=kind, warmup=warmup)
 
 
 def host_cpu_model():
@@ -461,13 +478,17 @@ def main():
         if out_sharded:  # 146 GB fp64 table does not fit the host: time a 16-output slice, scale by cost ~ n_out
             n_in0 = cfg["layers"][0][0]
             sl = pkg.Layer.random(n_in0, n_out0, G, seed=1000, gamma=1.0, device=local, out_range=(0, 16))
-            v, cores, sample, kind = cpu_reference(dict(cfg, layers=[(n_in0, 16)]), [sl.read_table()], budget_s=10)
-            v = v * 16 / n_out0
-            sample += f"; 16-output slice of the {n_out0}-output layer, samples/s scaled by 16/{n_out0} (cost is linear in n_out)"
+            r = cpu_reference(dict(cfg, layers=[(n_in0, 16)]), [sl.read_table()], budget_s=10)
+            scale = 16 / n_out0
+            extra = f"; 16-output slice of the {n_out0}-output layer, samples/s scaled by 16/{n_out0} (cost is linear in n_out)"
         else:
             tables = [lay.read_table() for lay in layers]
-            v, cores, sample, kind = cpu_reference(cfg, tables)
-        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind, "sample": sample,
+            r = cpu_reference(cfg, tables)
+            scale, extra = 1.0, ""
+        med = statistics.median(r["step_times"])
+        cpu = {"value": r["rows"] / med * scale, "unit": "samples/s", "cores": r["cores"], "kind": r["kind"],
+               "sample": f"{r['rows']} rows x {len(r['step_times'])} timed runs (median, {r['warmup']} warm-up) "
+                         f"of the {cfg['name']} workload" + extra,
                "cpu_model": host_cpu_model(), "threads_env": "LMKAN_THREADS=nproc"}
     fmas = B * sum(fma_per_row(a, b) for a, b in cfg["layers"])
     out = {
@@ -483,15 +504,10 @@ def main():
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic: X ~ N(0,1) (torch CUDA generator), table ~ N(0, 1/pairs) from a device counter RNG",
-        "config": {"workload": cfg["name"], "layers": cfg["layers"], "G": G, "batch_per_gpu": B,
-                   "global_batch": B if out_sharded else ws * B,
-                   "parallelism": (f"output-sharded over {shards} (this run: {ws} process(es); shard "
-                                   f"{rank % shards}, n_out_local={cfg['layers'][0][1]}"
-                                   f"{(', all-gather of Y columns fused into the epilogue (NVLink peer stores)' if args.gather == 'fused' else ', NCCL all-gather of Y columns') if ws > 1 else ', no all-gather: single-rank shard measurement'})"
-                                   if out_sharded else f"dp{ws} (batch rows, no collective)"),
-                   "l2": "inputs larger than L2: X %.0f MB, table %.0f MB vs 126 MB L2" % (
-                       B * cfg["layers"][0][0] * 4 / 1e6, sum(l.table_bytes for l in layers) / 1e6),
-                   "kernel_plan": plan},
+        "config": config_dict(CONFIGS[args.config], ws, rank, shards, args.gather),
+        "kernel_plan": dict(plan, n_out_local=cfg["layers"][0][1]),
+        "l2_policy": "inputs larger than L2: X %.0f MB, table %.0f MB vs 126 MB L2" % (
+            B * cfg["layers"][0][0] * 4 / 1e6, sum(l.table_bytes for l in layers) / 1e6),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(args.config),
                      "peak_source": peak_src, "kernel": "fwd_fused_kernel (gather; staged mode: K2)",
@@ -525,32 +541,39 @@ def main():
 
 def reference_arm(args, cfg, ws):
     """bench.py --impl reference: the reference's own CPU lmkan_forward
-    (oracle/_ref) on this host's cores, same workload/metric, bounded sample per step."""
+    (oracle/_ref) on this host's cores, same workload, metric and config
+    dict as the b200 arm. One step = one lmkan_forward pass over a bounded row
+    sample of the workload (sized so W + K steps take about 90 s); exactly W
+    untimed and K timed steps; ms_per_step / value are those of the sample
+    rows actually run (value = sample rows / median step time)."""
     import numpy as np
     G = cfg["G"]
     rng = np.random.default_rng(1000)
-    scale, run_cfg = 1.0, cfg
+    scale, run_cfg, extra = 1.0, cfg, ""
     if cfg.get("out_sharded"):  # the fp64 table (292 GB) does not fit the host: 16-output slice, scaled
         n_in0, n_out0 = cfg["layers"][0]
         run_cfg = dict(cfg, layers=[(n_in0, 16)])
         scale = 16 / n_out0
+        extra = f"; 16-output slice, samples/s scaled by {scale:g} (cost is linear in n_out)"
     tables = [(rng.standard_normal(((G + 1) ** 2 * (a // 2) * b)).astype(np.float32).astype(np.float64)
                / np.sqrt(a // 2)).reshape(G + 1, G + 1, a // 2, b) for a, b in run_cfg["layers"]]
-    budget = max(6.0, min(60.0, 2.0 * (args.steps + args.warmup)))
-    v, cores, sample, kind = cpu_reference(run_cfg, tables, budget_s=budget)
-    if scale != 1.0:
-        v *= scale
-        sample += f"; 16-output slice, samples/s scaled by {scale:g} (cost is linear in n_out)"
+    step_s = max(0.05, min(3.0, 90.0 / (args.steps + args.warmup)))
+    r = cpu_reference(run_cfg, tables, step_s=step_s, steps=args.steps, warmup=args.warmup)
+    med = statistics.median(r["step_times"])
+    v = r["rows"] / med * scale
+    sample = (f"each step: lmkan_forward over {r['rows']} of the workload's {cfg['batch']} rows "
+              f"({args.warmup} warm-up + {args.steps} timed steps, median){extra}")
+    shards = (args.shards or ws) if cfg.get("out_sharded") else 1
     out = {
         "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": cfg["batch"] / v * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+        "warmup": args.warmup, "ms_per_step": med * 1e3, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("out_sharded") else "weak", "vs_baseline": None, "dtype": "fp64",
         "data": "synthetic: X ~ N(0,1), table ~ N(0, 1/pairs), fp32-representable values widened to fp64",
-        "config": {"workload": cfg["name"], "layers": cfg["layers"], "G": G, "batch_per_gpu": cfg["batch"],
-                   "global_batch": cfg["batch"], "parallelism": "CPU threads (threading.hpp parallel_for)"},
+        "config": config_dict(cfg, ws, 0, shards, args.gather),
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": kind, "sample": sample,
-                         "cpu_model": host_cpu_model()},
+        "rows_per_step": r["rows"],
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": r["cores"], "kind": r["kind"], "sample": sample,
+                         "cpu_model": host_cpu_model(), "threads_env": "LMKAN_THREADS=nproc"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }

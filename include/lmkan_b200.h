@@ -184,6 +184,24 @@ int lmkan_b200_locate_f32(const lmkan_b200_layer* layer, const float* X_dev, int
 int lmkan_b200_locate_f64(const lmkan_b200_layer* layer, const double* X_dev, int32_t* i1,
                           int32_t* i2, float* w, int64_t rows, void* stream);
 
+/* Parity path for the PRODUCTION cell records (row_preambles, layer.hpp:96-101,
+ * as the gather kernels consume them; the cell index is cell_index_fast's fp32
+ * estimate verified against the thresholds). Per (row, pair), row-major
+ * [rows][pairs]: i1, i2 int32 and ag float2 {alpha, gamma} = fp32 of
+ * (points[i+1] - x) / (points[i+1] - points[i]) per axis (the gather forms the
+ * reference weights w00 = alpha*gamma, w10 = (1-alpha)*gamma, w01 = alpha*(1-gamma),
+ * w11 = (1-alpha)*(1-gamma) from them). variant 0: the output of K1
+ * (records4_kernel) for the layer's staged plan at `rows`, decoded from where
+ * K2 reads it (packed slab/node offsets + {alpha, gamma} rings); 1: the same
+ * from the shared-memory-tile K1 (records_kernel); 2: the in-kernel locate of
+ * the fused / global / narrow gather kernels (same shared-memory constants,
+ * node stride and slab height). EINVAL for variants 0/1 on narrow (n_out <= 4)
+ * layers. Device pointers; asynchronous on `stream`. */
+int lmkan_b200_records_f32(const lmkan_b200_layer* layer, const float* X_dev, int32_t* i1, int32_t* i2,
+                           float* ag, int64_t rows, int variant, void* stream);
+int lmkan_b200_records_f64(const lmkan_b200_layer* layer, const double* X_dev, int32_t* i1, int32_t* i2,
+                           float* ag, int64_t rows, int variant, void* stream);
+
 /* Tuning / introspection: kernel variant chosen for `rows` (OT = output tile,
  * RT = rows per thread, NBUF = sheet buffers, rows_per_cta = the row tile,
  * possibly shortened so the grid fills whole waves of SMs), the number of

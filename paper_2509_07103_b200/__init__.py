@@ -247,6 +247,25 @@ class Layer:
         check(fn(self._h, _ptr(X), _ptr(i1), _ptr(i2), _ptr(w), int(rows), _stream_ptr(stream)))
         return i1, i2, w
 
+    RECORD_VARIANTS = {"k1": 0, "k1_smem": 1, "in_kernel": 2}
+
+    def records(self, X, variant: str = "k1", stream=None):
+        """The PRODUCTION cell records (what the gather kernels consume), decoded:
+        (i1, i2, ag) CUDA tensors [rows, pairs] / [rows, pairs, 2] with
+        ag = {alpha, gamma}. variant: "k1" (records4_kernel of the staged plan),
+        "k1_smem" (records_kernel), "in_kernel" (fused / global / narrow locate)."""
+        import torch
+        assert X.is_cuda and X.is_contiguous() and X.dim() == 2 and X.shape[1] == self.n_in
+        assert X.dtype in (torch.float32, torch.float64)
+        rows = X.shape[0]
+        i1 = torch.empty((rows, self.pairs), dtype=torch.int32, device=X.device)
+        i2 = torch.empty_like(i1)
+        ag = torch.empty((rows, self.pairs, 2), dtype=torch.float32, device=X.device)
+        fn = lib.lmkan_b200_records_f32 if X.dtype == torch.float32 else lib.lmkan_b200_records_f64
+        check(fn(self._h, _ptr(X), _ptr(i1), _ptr(i2), _ptr(ag), int(rows), self.RECORD_VARIANTS[variant],
+                 _stream_ptr(stream)))
+        return i1, i2, ag
+
     # -- training path ------------------------------------------------------
     def backward(self, P, X, dY, dP=None, want_dx: bool = True, workers: int = 0, stream=None):
         """lmkan_backward (layer.hpp:141-202) in fp64. CUDA tensors: P (the fp64

@@ -52,6 +52,8 @@ _SIGS = [
     ("lmkan_b200_forward_host_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
     ("lmkan_b200_locate_f32", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),
     ("lmkan_b200_locate_f64", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),
+    ("lmkan_b200_records_f32", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.c_int, _P]),
+    ("lmkan_b200_records_f64", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.c_int, _P]),
     ("lmkan_b200_plan", C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("lmkan_b200_lane_vectors", C.c_int, [C.c_int]),
     ("lmkan_b200_backward_f64", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int64, C.c_uint64, _P]),

@@ -295,6 +295,71 @@ __global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X,
     }
 }
 
+// ---------------------------------------------------- parity / debug views
+// The PRODUCTION cell records decoded back into row_preambles' terms
+// (layer.hpp:96-101): per (row, pair) the cell (i1, i2) and {alpha, gamma}.
+// Packed offset = (slab << 24) | (node-within-slab * NS), node = i1'(G+1) + i2.
+__device__ __forceinline__ void decode_packed(int packed, int G, int H, int NS, int& i1, int& i2) {
+    const int s = packed >> kSlabShift;
+    const int nodews = (packed & kOffMask) / NS;
+    i1 = s * H + nodews / (G + 1);
+    i2 = nodews % (G + 1);
+}
+
+// Reads K1's output (W[p][rows_pad], O[p][tile][offset_slot]) exactly where K2
+// reads it: one thread per (row, pair), row-major over [rows][pairs].
+static __global__ void __launch_bounds__(256) decode_records_kernel(const float2* __restrict__ W, const int* __restrict__ O,
+                                                             int64_t rows, int64_t rows_pad, int pairs, ShapeRT sh,
+                                                             int64_t Rt, int G, int H, int32_t* __restrict__ o_i1,
+                                                             int32_t* __restrict__ o_i2, float2* __restrict__ o_ag) {
+    const int64_t tiles = rows_pad / Rt;
+    const int64_t total = rows * pairs;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = k / pairs;
+        const int p = static_cast<int>(k - r * pairs);
+        const int64_t tile = r / Rt;
+        const int slot = offset_slot(sh, static_cast<int>(r - tile * Rt));
+        int i1, i2;
+        decode_packed(O[(static_cast<size_t>(p) * tiles + tile) * sh.OBLK + slot], G, H, sh.NS, i1, i2);
+        o_i1[k] = i1;
+        o_i2[k] = i2;
+        o_ag[k] = W[static_cast<size_t>(p) * rows_pad + r];
+    }
+}
+
+// The in-kernel locate of the fused / global gather modes and the narrow kernel
+// (locate_ag on the same shared-memory grid constants, same node stride NS and
+// slab height H), one thread per (row, pair), decoded like decode_records_kernel.
+template <typename XT>
+__global__ void __launch_bounds__(256) locate_ag_kernel(const XT* __restrict__ X, int64_t rows, int n_in,
+                                                        const __grid_constant__ GridConst gc, int NS, int H,
+                                                        int32_t* __restrict__ o_i1, int32_t* __restrict__ o_i2,
+                                                        float2* __restrict__ o_ag) {
+    __shared__ XT thr[kMaxThr];
+    __shared__ double pts[kMaxThr + 1];
+    __shared__ double invh[kMaxThr];
+    const int G = gc.G;
+    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = threadIdx.x; k <= G; k += blockDim.x) pts[k] = gc.points[k];
+    for (int k = threadIdx.x; k < G; k += blockDim.x) invh[k] = gc.inv_h[k];
+    __syncthreads();
+    const int pairs = n_in / 2;
+    const int64_t total = rows * pairs;
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = k / pairs;
+        const int p = static_cast<int>(k - r * pairs);
+        const XT* xr = X + r * n_in + 2 * p;
+        float2 ag;
+        int i1, i2;
+        decode_packed(locate_ag<XT>(xr[0], xr[1], thr, pts, invh, G, gc.L, NS, H, ag), G, H, NS, i1, i2);
+        o_i1[k] = i1;
+        o_i2[k] = i2;
+        o_ag[k] = ag;
+    }
+}
+
 // K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
 // Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
 // [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of

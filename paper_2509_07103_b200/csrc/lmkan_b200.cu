@@ -140,7 +140,7 @@ bool choose_dup(int OT, int G, int smem_cap) {
 // otherwise; global-sheet fallback when nothing fits shared memory.
 // Within a mode: prefer double buffering with the fewest slabs, then the
 // largest row tile that still fills the GPU with one wave of CTAs.
-bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out) {
+bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out, int force_mode_arg = -1) {
     // ring depth: up to 4 (deeper rings measured no faster at cfg1-4; LMKAN_B200_MAX_NBUF overrides)
     const int max_nbuf = std::max(2, std::min(16, env_int("LMKAN_B200_MAX_NBUF", 4)));
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
@@ -151,8 +151,8 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out)
                    rows, 1, 0};
         return static_cast<int>(out.smem) <= smem_cap;
     }
-    int force_mode = -1;
-    if (const char* e = std::getenv("LMKAN_B200_MODE")) {
+    int force_mode = force_mode_arg;
+    if (const char* e = force_mode_arg >= 0 ? nullptr : std::getenv("LMKAN_B200_MODE")) {
         if (!std::strcmp(e, "fused")) force_mode = kModeFused;
         if (!std::strcmp(e, "staged")) force_mode = kModeStaged;
         if (!std::strcmp(e, "global")) force_mode = kModeGlobal;
@@ -270,6 +270,39 @@ struct ChainLink {
     const GridConst* gc_next = nullptr;
 };
 
+// K1: the cell records of `rows` rows in K2's order (records4_kernel, or the
+// shared-memory-tile records_kernel when reg4 is false).
+template <typename XT>
+void launch_records(const lmkan_b200_layer* L, const Plan& pl, const XT* X, int64_t rows, const InputMap& im,
+                    float2* recW, int* recO, bool reg4, cudaStream_t st) {
+    const int H = (L->G + pl.S - 1) / pl.S;
+    if (reg4) {  // register-direct K1 (records4_kernel)
+        const int64_t py = (L->pairs + 3) / 4;
+        const int64_t gx = std::min<int64_t>((pl.rows_pad + 255) / 256,
+                                             std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
+        dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
+        // 32-byte group loads: 8 contiguous inputs at 32-byte aligned offsets
+        const bool vec = (reinterpret_cast<uintptr_t>(X) & 31) == 0 &&
+                         (im.conv ? (im.C % 8 == 0) : (L->n_in % 8 == 0));
+        if (pl.row_tile < pl.sh.R)
+            records4_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
+                                                          recO, im, pl.row_tile, vec ? 1 : 0);
+        else
+            records4_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
+                                                           recO, im, pl.row_tile, vec ? 1 : 0);
+    } else {
+        const int64_t py = (L->pairs + 15) / 16;
+        const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
+        dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
+        if (pl.row_tile < pl.sh.R)
+            records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                         im, pl.row_tile);
+        else
+            records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
+                                                          im, pl.row_tile);
+    }
+}
+
 template <typename XT>
 int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                  const InputMap& im,
@@ -295,32 +328,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
             cudaFreeAsync(recW, st);
             return cuda_fail(e, "lmkan_forward: record scratch");
         }
-        const int H = (L->G + pl.S - 1) / pl.S;
-        if (env_int("LMKAN_B200_K1", 4) == 4) {  // register-direct K1 (records4_kernel)
-            const int64_t py = (L->pairs + 3) / 4;
-            const int64_t gx = std::min<int64_t>((pl.rows_pad + 255) / 256,
-                                                 std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
-            dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
-            // 32-byte group loads: 8 contiguous inputs at 32-byte aligned offsets
-            const bool vec = (reinterpret_cast<uintptr_t>(X) & 31) == 0 &&
-                             (im.conv ? (im.C % 8 == 0) : (L->n_in % 8 == 0));
-            if (pl.row_tile < pl.sh.R)
-                records4_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
-                                                              recO, im, pl.row_tile, vec ? 1 : 0);
-            else
-                records4_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
-                                                               recO, im, pl.row_tile, vec ? 1 : 0);
-        } else {
-            const int64_t py = (L->pairs + 15) / 16;
-            const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
-            dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
-            if (pl.row_tile < pl.sh.R)
-                records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                             im, pl.row_tile);
-            else
-                records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                              im, pl.row_tile);
-        }
+        launch_records<XT>(L, pl, X, rows, im, recW, recO, env_int("LMKAN_B200_K1", 4) == 4, st);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(recW, st);
@@ -412,6 +420,58 @@ int locate_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t* 
     return LMKAN_B200_OK;
 }
 
+// Production cell records decoded per (row, pair) (lmkan_b200_records_*):
+// variant 0/1 = K1 (records4_kernel / records_kernel) of the layer's staged
+// plan for `rows`, read back where K2 reads them; 2 = the in-kernel locate of
+// the fused / global / narrow gather kernels.
+template <typename XT>
+int records_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t* i2, float* ag, int64_t rows,
+                   int variant, cudaStream_t st) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "records: null layer");
+    if (rows <= 0) return rows == 0 ? LMKAN_B200_OK : fail(LMKAN_B200_EINVAL, "records: negative rows");
+    if (!X || !i1 || !i2 || !ag || reinterpret_cast<uintptr_t>(ag) % 8 != 0)
+        return fail(LMKAN_B200_EINVAL, "records: null or misaligned output");
+    if (variant < 0 || variant > 2) return fail(LMKAN_B200_EINVAL, "records: variant must be 0, 1 or 2");
+    if (variant < 2 && L->narrow) return fail(LMKAN_B200_EINVAL, "records: narrow layers have no K1 records");
+    DeviceGuard g(L->device);
+    const int cap = max_smem_optin(L->device);
+    const int64_t total = rows * L->pairs;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, kNumSMs * 16));
+    float2* out_ag = reinterpret_cast<float2*>(ag);
+    if (variant == 2) {
+        int H = L->G;
+        if (!L->narrow) {
+            Plan pl;
+            if (!make_plan(L, rows, cap, pl, kModeFused) && !make_plan(L, rows, cap, pl, kModeGlobal))
+                return fail(LMKAN_B200_EINVAL, "records: no fused plan");
+            H = (L->G + pl.S - 1) / pl.S;
+        }
+        locate_ag_kernel<XT><<<blocks, 256, 0, st>>>(X, rows, L->n_in, L->gc, L->ns, H, i1, i2, out_ag);
+        CK(cudaGetLastError());
+        return LMKAN_B200_OK;
+    }
+    Plan pl;
+    if (!make_plan(L, rows, cap, pl, kModeStaged)) return fail(LMKAN_B200_EINVAL, "records: no staged plan");
+    float2* recW = nullptr;
+    int* recO = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&recW), static_cast<size_t>(L->pairs) * pl.rows_pad * sizeof(float2), st));
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&recO),
+                                    static_cast<size_t>(L->pairs) * pl.row_tiles * pl.sh.OBLK * sizeof(int), st);
+    if (e == cudaSuccess) {
+        launch_records<XT>(L, pl, X, rows, InputMap{}, recW, recO, variant == 0, st);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        decode_records_kernel<<<blocks, 256, 0, st>>>(recW, recO, rows, pl.rows_pad, L->pairs, pl.sh, pl.row_tile, L->G,
+                                                      (L->G + pl.S - 1) / pl.S, i1, i2, out_ag);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(recW, st);
+    if (recO) cudaFreeAsync(recO, st);
+    if (e != cudaSuccess) return cuda_fail(e, "records");
+    return LMKAN_B200_OK;
+}
+
 int validate_shape(int n_in, int n_out, int G) {
     if (n_in <= 0 || n_in % 2 != 0)
         return fail(LMKAN_B200_EINVAL, "init_layer: n_in must be a positive even number");
@@ -472,7 +532,12 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
     if (e == cudaSuccess)
         e = cudaMemcpy(L->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&L->table, L->table_bytes);
+    // the allocation is rounded up to 16 B and the tail zeroed: the narrow kernel
+    // bulk-copies the whole table, and bulk copies move multiples of 16 B
+    const size_t alloc_bytes = (L->table_bytes + 15) & ~static_cast<size_t>(15);
+    if (e == cudaSuccess) e = cudaMalloc(&L->table, alloc_bytes);
+    if (e == cudaSuccess && alloc_bytes > L->table_bytes)
+        e = cudaMemset(reinterpret_cast<char*>(L->table) + L->table_bytes, 0, alloc_bytes - L->table_bytes);
     if (e != cudaSuccess) {
         cudaFree(L->d_inv);
         delete L;
@@ -968,6 +1033,15 @@ int lmkan_b200_locate_f32(const lmkan_b200_layer* L, const float* X, int32_t* i1
 int lmkan_b200_locate_f64(const lmkan_b200_layer* L, const double* X, int32_t* i1, int32_t* i2, float* w,
                           int64_t rows, void* stream) {
     return locate_device<double>(L, X, i1, i2, w, rows, static_cast<cudaStream_t>(stream));
+}
+
+int lmkan_b200_records_f32(const lmkan_b200_layer* L, const float* X, int32_t* i1, int32_t* i2, float* ag,
+                           int64_t rows, int variant, void* stream) {
+    return records_device<float>(L, X, i1, i2, ag, rows, variant, static_cast<cudaStream_t>(stream));
+}
+int lmkan_b200_records_f64(const lmkan_b200_layer* L, const double* X, int32_t* i1, int32_t* i2, float* ag,
+                           int64_t rows, int variant, void* stream) {
+    return records_device<double>(L, X, i1, i2, ag, rows, variant, static_cast<cudaStream_t>(stream));
 }
 
 int lmkan_b200_lane_vectors(int out_tile) { return lane_vectors(out_tile); }

@@ -29,9 +29,11 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
                   const InputMap im) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G, pairs = n_in / 2, nodes = (G + 1) * (G + 1);
-    const uint32_t tab_bytes = static_cast<uint32_t>(nodes) * pairs * NO * 4u;
+    // bulk copies move multiples of 16 B: the copy includes the table
+    // allocation's zeroed tail (alloc_layer rounds it up to 16 B)
+    const uint32_t tab_bytes = (static_cast<uint32_t>(nodes) * pairs * NO * 4u + 15u) & ~15u;
     float* tab = reinterpret_cast<float*>(smem);
-    uint32_t o = (tab_bytes + 15u) & ~15u;
+    uint32_t o = tab_bytes;
     XT* thr = reinterpret_cast<XT*>(smem + o);
     o += kMaxThr * 8u;
     double* pts = reinterpret_cast<double*>(smem + o);

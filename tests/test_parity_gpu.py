@@ -353,7 +353,10 @@ def test_cfg5_shape_output_slice(torch, pkg, oracle):
 
 
 @pytest.mark.parametrize("n_in,n_out,G,rows", [(128, 1, 28, 3000), (64, 2, 16, 2000), (30, 3, 8, 999),
-                                               (2, 4, 5, 100), (200, 1, 12, 513)])
+                                               (2, 4, 5, 100), (200, 1, 12, 513),
+                                               # tables whose byte size is not a multiple of 16 (the bulk
+                                               # copy moves the allocation's zeroed 16-B-rounded tail)
+                                               (2, 1, 4, 77), (6, 1, 8, 300), (10, 2, 4, 129), (14, 2, 6, 64)])
 def test_narrow_kernel(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows):
     """n_out <= 4 layers run the narrow kernel (whole table in shared memory,
     one row per lane); parity vs the oracle, bitwise vs the padded general path."""
