@@ -17,6 +17,7 @@ struct lmkan_b200_layer {
     bool narrow = false;  // n_out <= 4: [pair][node][OT] table, K4 narrow kernel
     bool dup = false;     // OT = 16 duplicated-node table [ot][pair][node][2][OT] (conflict-free gathers)
     int ns = 64;          // node stride of the device table in floats (OT, or 2 OT when dup)
+    int pair_block = 0;   // pair-block summation block (0: one running sum; see fwd_fused_kernel)
     float* table = nullptr;
     size_t table_bytes = 0;
     double* d_inv = nullptr;

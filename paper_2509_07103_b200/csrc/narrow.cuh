@@ -26,7 +26,7 @@ template <typename XT, int NO>
 __global__ void __launch_bounds__(kNarrowThreads, 1)
     narrow_kernel(const XT* __restrict__ X, const OutDests<XT> out, int64_t rows, int n_in, int n_out,
                   const float* __restrict__ table, float gamma, const __grid_constant__ GridConst gc,
-                  const InputMap im) {
+                  const InputMap im, int pair_block) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G, pairs = n_in / 2, nodes = (G + 1) * (G + 1);
     // bulk copies move multiples of 16 B: the copy includes the table
@@ -66,11 +66,18 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
     const bool vec8 = vec4 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;
     for (int64_t r = static_cast<int64_t>(blockIdx.x) * kNarrowThreads + tid; r < rows;
          r += static_cast<int64_t>(gridDim.x) * kNarrowThreads) {
-        float acc[NO];
+        float acc[NO], run[NO];  // run: pair-block running sum (fwd_fused_kernel's fold_main, in registers)
 #pragma unroll
-        for (int q = 0; q < NO; ++q) acc[q] = 0.f;
+        for (int q = 0; q < NO; ++q) acc[q] = run[q] = 0.f;
         const XT* xr = X + in_rowbase(im, r, n_in);
         auto one_pair = [&](int p, XT x1, XT x2) {
+            if (pair_block > 0 && p > 0 && p % pair_block == 0) {
+#pragma unroll
+                for (int q = 0; q < NO; ++q) {
+                    run[q] = run[q] + acc[q];
+                    acc[q] = 0.f;
+                }
+            }
             float2 ag;
             const int off = locate_ag<XT>(x1, x2, thr, pts, inv, G, gc.L, NO, G, ag);
             const float4 w = weights_ag(ag);
@@ -100,6 +107,10 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
             }
         }
         for (; p < pairs; ++p) one_pair(p, xr[in_coloff(im, 2 * p)], xr[in_coloff(im, 2 * p + 1)]);
+        if (pair_block > 0 && pairs > pair_block) {
+#pragma unroll
+            for (int q = 0; q < NO; ++q) acc[q] = run[q] + acc[q];
+        }
 #pragma unroll
         for (int d = 0; d < kMaxDest; ++d) {
             if (d >= out.n) break;

@@ -38,3 +38,15 @@ def oracle():
 def port():
     import pyoracle
     return pyoracle.Port()
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2509_07103_b200 as p
+    return p
