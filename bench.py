@@ -462,6 +462,32 @@ def main():
                "ms_per_step": dt * 1e3,
                "timer": "host wall clock around H2D + forward + D2H + host read (public API)"}
 
+    # ---- e2e through the reference-signature C++ drop-in (tools/dropin_bench):
+    # lmkan_b200::lmkan_forward(const LmKanLayer&, const Matrix&, Matrix&), fp64
+    # X / Y in pageable host memory, exactly what an existing caller of
+    # lmkan::lmkan_forward (layer.hpp:108-134) runs after the namespace swap.
+    e2e_dropin = None
+    dropin_bin = os.path.join(ROOT, "tools", "dropin_bench")
+    if (not args.no_e2e and len(cfg["layers"]) == 1 and not conv and not out_sharded
+            and os.path.exists(dropin_bin)):
+        n_in0, n_out0 = cfg["layers"][0]
+        Kd = max(3, min(K, 10))
+        r = subprocess.run([dropin_bin, str(n_in0), str(n_out0), str(G), str(B), str(Kd), "2", str(local)],
+                           capture_output=True, text=True, timeout=900)
+        if r.returncode == 0:
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            td = torch.tensor([d["ms_per_step"]], device=f"cuda:{local}")
+            if dist:
+                dist.all_reduce(td, op=dist.ReduceOp.MAX)
+            e2e_dropin = {"value": ws * B / (float(td.item()) / 1e3), "unit": "samples/s",
+                          "h2d_bytes_per_step": d["h2d_bytes_per_step"], "d2h_bytes_per_step": d["d2h_bytes_per_step"],
+                          "ms_per_step": float(td.item()), "steps": d["steps"],
+                          "api": "lmkan_b200::lmkan_forward(const LmKanLayer&, const Matrix&, Matrix&): fp64 X/Y in "
+                                 "pageable host memory (tools/dropin_bench.cpp)",
+                          "timer": "host wall clock per call, Y on the host when it returns"}
+        else:
+            e2e_dropin = {"error": (r.stderr or r.stdout)[-300:]}
+
     if rank != 0:
         if peers is not None:
             peers.close()
@@ -528,6 +554,7 @@ def main():
                      "levels": roofline_levels(achieved, fmas / (kernel_ms / 1e3), peak, clocks.get("sm_mhz"))},
         "clocks": clocks,
         "e2e": e2e,
+        "e2e_dropin": e2e_dropin,
         "cpu_baseline": cpu,
         "gpu_launches": K * launches_per_step,
         "impl": "b200",

@@ -21,9 +21,9 @@
 // compute path: lmkan_forward runs on the layer's GPU (LmKanLayer::device).
 //
 // The layer keeps a prepared device table (fp32, [out_tile][pair][node][OT])
-// next to the host P. It is rebuilt whenever P or the shape changed since the
-// last forward (a 64-bit fingerprint of the whole table is checked per call);
-// call freeze() to promise P will not change and skip the fingerprint.
+// next to the host P. It is rebuilt whenever P may have changed since the last
+// forward (P is a ParamVector: non-const access bumps a generation counter, an
+// O(1) check per call) or the shape / device changed.
 #pragma once
 
 #include <algorithm>
@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -142,41 +143,106 @@ inline Preamble preamble(const SigmaGrid& grid, double x1, double x2) {
     return r;
 }
 
+// std::vector<double> with a mutation generation, the type of LmKanLayer::P.
+// Every non-const access (element references, data(), iterators, assign /
+// resize / clear / push_back, assignment, and the conversion to
+// std::vector<double>& used by functions taking the reference's vector)
+// bumps the generation; const access does not. lmkan_forward re-uploads the
+// device table only when the generation moved since the last upload: O(1)
+// per call instead of hashing P. Writes through a pointer or iterator taken
+// BEFORE a forward and used after it are not seen; take it again (as the
+// reference's own optimizer does every step, model.hpp:382-386) or call
+// touch().
+class ParamVector {
+public:
+    using vector_type = std::vector<double>;
+    using value_type = double;
+    using size_type = std::size_t;
+    using iterator = vector_type::iterator;
+    using const_iterator = vector_type::const_iterator;
+
+    ParamVector() = default;
+    explicit ParamVector(size_type n, double v = 0.0) : v_(n, v) {}
+    ParamVector(std::initializer_list<double> l) : v_(l) {}
+    ParamVector(const vector_type& v) : v_(v) {}
+    ParamVector(vector_type&& v) : v_(std::move(v)) {}
+    ParamVector(const ParamVector& o) : v_(o.v_) {}
+    ParamVector(ParamVector&& o) noexcept : v_(std::move(o.v_)) { o.touch(); }
+    ParamVector& operator=(const ParamVector& o) {
+        v_ = o.v_;
+        touch();
+        return *this;
+    }
+    ParamVector& operator=(ParamVector&& o) noexcept {
+        v_ = std::move(o.v_);
+        touch();
+        o.touch();
+        return *this;
+    }
+    ParamVector& operator=(vector_type v) {
+        v_ = std::move(v);
+        touch();
+        return *this;
+    }
+
+    // const access: no generation change
+    size_type size() const { return v_.size(); }
+    bool empty() const { return v_.empty(); }
+    const double* data() const { return v_.data(); }
+    const double& operator[](size_type i) const { return v_[i]; }
+    const double& at(size_type i) const { return v_.at(i); }
+    const double& front() const { return v_.front(); }
+    const double& back() const { return v_.back(); }
+    const_iterator begin() const { return v_.begin(); }
+    const_iterator end() const { return v_.end(); }
+    const_iterator cbegin() const { return v_.cbegin(); }
+    const_iterator cend() const { return v_.cend(); }
+    operator const vector_type&() const { return v_; }
+    const vector_type& vec() const { return v_; }
+
+    // mutable access: bumps the generation
+    double* data() { return touch(), v_.data(); }
+    double& operator[](size_type i) { return touch(), v_[i]; }
+    double& at(size_type i) { return touch(), v_.at(i); }
+    double& front() { return touch(), v_.front(); }
+    double& back() { return touch(), v_.back(); }
+    iterator begin() { return touch(), v_.begin(); }
+    iterator end() { return touch(), v_.end(); }
+    operator vector_type&() { return touch(), v_; }
+    vector_type& vec() { return touch(), v_; }
+    void assign(size_type n, double v) { touch(), v_.assign(n, v); }
+    template <class It>
+    void assign(It a, It b) { touch(), v_.assign(a, b); }
+    void resize(size_type n, double v = 0.0) { touch(), v_.resize(n, v); }
+    void clear() { touch(), v_.clear(); }
+    void push_back(double v) { touch(), v_.push_back(v); }
+    void swap(ParamVector& o) { touch(), o.touch(), v_.swap(o.v_); }
+    void swap(vector_type& o) { touch(), v_.swap(o); }
+
+    std::uint64_t generation() const { return gen_; }
+    void touch() { ++gen_; }
+
+    friend bool operator==(const ParamVector& a, const ParamVector& b) { return a.v_ == b.v_; }
+    friend bool operator!=(const ParamVector& a, const ParamVector& b) { return a.v_ != b.v_; }
+    friend bool operator==(const ParamVector& a, const vector_type& b) { return a.v_ == b; }
+    friend bool operator!=(const ParamVector& a, const vector_type& b) { return a.v_ != b; }
+
+private:
+    vector_type v_;
+    std::uint64_t gen_ = 0;
+};
+
 namespace detail {
 struct Prepared {
     lmkan_b200_layer* h = nullptr;
     int n_in = 0, n_out = 0, G = 0, device = 0;
-    std::uint64_t fingerprint = 0;
+    const double* data = nullptr;
+    std::size_t size = 0;
+    std::uint64_t generation = 0;
     ~Prepared() {
         if (h) lmkan_b200_layer_destroy(h);
     }
 };
-
-inline std::uint64_t fingerprint(const std::vector<double>& P) {
-    // four independent multiply / xor-shift lanes over the raw 64-bit words
-    // (the xor-shift carries every bit, including sign flips, into later rounds)
-    const std::uint64_t k = 0x9e3779b97f4a7c15ull;
-    std::uint64_t a = 1, b = 2, c = 3, d = 4;
-    const std::size_t n = P.size();
-    std::size_t i = 0;
-    auto word = [&](std::size_t j) {
-        std::uint64_t u;
-        std::memcpy(&u, &P[j], 8);
-        return u;
-    };
-    auto mix = [&](std::uint64_t h, std::uint64_t w) {
-        h = (h ^ w) * k;
-        return h ^ (h >> 29);
-    };
-    for (; i + 4 <= n; i += 4) {
-        a = mix(a, word(i));
-        b = mix(b, word(i + 1));
-        c = mix(c, word(i + 2));
-        d = mix(d, word(i + 3));
-    }
-    for (; i < n; ++i) a = mix(a, word(i));
-    return mix(mix(mix(mix(n, a), b), c), d);
-}
 }  // namespace detail
 
 // layer.hpp:24-61. Same public fields and the same P layout
@@ -185,7 +251,7 @@ struct LmKanLayer {
     int n_in = 0;
     int n_out = 0;
     SigmaGrid grid;
-    std::vector<double> P;
+    ParamVector P;  // std::vector<double> semantics; tracks modifications (see ParamVector)
     double gamma = 0.0;
     int device = 0;
 
@@ -198,7 +264,6 @@ struct LmKanLayer {
         if (this != &o) {
             n_in = o.n_in; n_out = o.n_out; grid = o.grid; P = o.P; gamma = o.gamma; device = o.device;
             cache_.reset();
-            frozen_ = false;
         }
         return *this;
     }
@@ -218,21 +283,22 @@ struct LmKanLayer {
         return P.data() + node_offset(i1, i2) + static_cast<std::size_t>(pair) * n_out;
     }
 
-    // Promise that P will not change any more: forward skips the fingerprint.
-    void freeze() { frozen_ = true; }
     // Drop the device table (e.g. to free GPU memory); rebuilt on next use.
     void release() const { cache_.reset(); }
 
-    // The prepared device handle, (re)built if P changed since the last call.
+    // The prepared device handle, (re)built when P was (possibly) modified
+    // since the last call (ParamVector generation), or the shape / device changed.
     lmkan_b200_layer* prepared() const {
-        const std::uint64_t fp = (frozen_ && cache_) ? cache_->fingerprint : detail::fingerprint(P);
-        if (!cache_ || cache_->fingerprint != fp || cache_->n_in != n_in || cache_->n_out != n_out ||
+        if (!cache_ || cache_->generation != P.generation() || cache_->data != P.data() ||
+            cache_->size != P.size() || cache_->n_in != n_in || cache_->n_out != n_out ||
             cache_->G != grid.G || cache_->device != device) {
             auto pr = std::make_shared<detail::Prepared>();
             detail::throw_status(
                 lmkan_b200_layer_create(n_in, n_out, grid.G, gamma, P.data(), device, &pr->h), "lmkan_forward");
             pr->n_in = n_in; pr->n_out = n_out; pr->G = grid.G; pr->device = device;
-            pr->fingerprint = fp;
+            pr->data = P.data();
+            pr->size = P.size();
+            pr->generation = P.generation();
             cache_ = std::move(pr);
         }
         detail::throw_status(lmkan_b200_layer_set_gamma(cache_->h, gamma), "lmkan_forward");
@@ -241,7 +307,6 @@ struct LmKanLayer {
 
 private:
     mutable std::shared_ptr<detail::Prepared> cache_;
-    bool frozen_ = false;
 };
 
 // costs.hpp:14-29: main-term FMA count (k^d / d) * n_in * n_out and the

@@ -14,11 +14,28 @@
 // time, lost ~20% to that.) Two compute streams let the next chunk's CTAs fill
 // the SMs left idle by the last partial wave of the current one (one compute
 // stream cost cfg2's host path 19% of its e2e throughput).
+//
+// Pageable (ordinary malloc / std::vector) host buffers — the reference
+// signature's Matrix — are staged through pinned slots: a pool of host threads
+// copies chunk c+1's X into its pinned slot and chunk c-1's Y out of its slot
+// while the GPU works on chunk c, so the copies still overlap (a
+// cudaMemcpyAsync straight from pageable memory is synchronous, single-threaded
+// and bounced through the driver's own small pinned buffer).
 #pragma once
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 #include <cuda_runtime.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 namespace lmkan_b200 {
 
@@ -49,6 +66,141 @@ struct ChunkSchedule {
     int64_t size(int64_t c) const { return start[c + 1] - start[c]; }
 };
 
+// Parallel host copies over a persistent pool of threads (the caller takes a
+// share too). LMKAN_B200_COPY_THREADS overrides the pool size (default: the
+// hardware threads, at most 32).
+class CopyPool {
+public:
+    CopyPool() = default;
+    CopyPool(const CopyPool&) = delete;
+    CopyPool& operator=(const CopyPool&) = delete;
+    ~CopyPool() { stop(); }
+
+    // Both copies stream their stores past the caches (non-temporal), so the
+    // destination is not read first: the pageable path is bound by host memory
+    // bandwidth (tools/ubench_hostcopy.cpp), and every byte not moved counts.
+    void copy(void* dst, const void* src, size_t bytes) {
+        char* d = static_cast<char*>(dst);
+        const char* s = static_cast<const char*>(src);
+        parallel(bytes, 64, [=](size_t lo, size_t hi) { copy_nt(d + lo, s + lo, hi - lo); });
+    }
+    // dst[i] = double(src[i]): fp32 results widened into the caller's fp64 Y
+    void widen(double* dst, const float* src, size_t count) {
+        parallel(count, 16, [=](size_t lo, size_t hi) { widen_nt(dst + lo, src + lo, hi - lo); });
+    }
+
+    static void copy_nt(char* d, const char* s, size_t n) {
+#if defined(__SSE2__)
+        size_t i = 0;
+        for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = s[i];
+        for (; i + 64 <= n; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+            const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+        }
+        _mm_sfence();
+        if (i < n) std::memcpy(d + i, s + i, n - i);
+#else
+        std::memcpy(d, s, n);
+#endif
+    }
+    static void widen_nt(double* d, const float* s, size_t n) {
+        size_t i = 0;
+#if defined(__SSE2__)
+        for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = static_cast<double>(s[i]);
+        for (; i + 4 <= n; i += 4) {
+            const __m128 v = _mm_loadu_ps(s + i);
+            _mm_stream_pd(d + i, _mm_cvtps_pd(v));
+            _mm_stream_pd(d + i + 2, _mm_cvtps_pd(_mm_movehl_ps(v, v)));
+        }
+        _mm_sfence();
+#endif
+        for (; i < n; ++i) d[i] = static_cast<double>(s[i]);
+    }
+
+private:
+    template <class F>
+    void parallel(size_t n, size_t align, F fn) {
+        start();
+        const size_t t = workers_.size() + 1;
+        if (n < (size_t(1) << 18) || t == 1) {
+            fn(0, n);
+            return;
+        }
+        const size_t part = ((n + t - 1) / t + align - 1) / align * align;
+        auto run_part = [=](size_t k) {
+            const size_t lo = k * part;
+            if (lo < n) fn(lo, std::min(n, lo + part));
+        };
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_fn_ = run_part;
+            pending_ = workers_.size();
+            ++job_;
+        }
+        cv_.notify_all();
+        run_part(t - 1);  // the caller's share
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+    void start() {
+        if (started_) return;
+        started_ = true;
+        // all hardware threads (measured on a 16-core host: 4 / 8 / 16 threads
+        // -> pageable cfg2 drop-in 47 / 34 / 28 ms per call)
+        int n = static_cast<int>(std::thread::hardware_concurrency());
+        if (const char* e = std::getenv("LMKAN_B200_COPY_THREADS")) n = std::atoi(e);
+        n = std::max(1, std::min(n, 32));
+        for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this, i] { run(static_cast<size_t>(i)); });
+    }
+    void stop() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            quit_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+        workers_.clear();
+    }
+    void run(size_t idx) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return quit_ || job_ != seen; });
+            if (quit_) return;
+            seen = job_;
+            std::function<void(size_t)> fn = job_fn_;
+            lk.unlock();
+            fn(idx);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    bool started_ = false, quit_ = false;
+    uint64_t job_ = 0;
+    size_t pending_ = 0;
+    std::function<void(size_t)> job_fn_;
+};
+
+// true when p is ordinary pageable host memory (not pinned / registered / managed)
+inline bool is_pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
 struct HostPipeline {
     static constexpr int kSlots = 3;
     int device = -1;
@@ -57,6 +209,10 @@ struct HostPipeline {
     void* dX[kSlots] = {};
     void* dY[kSlots] = {};
     size_t xcap = 0, ycap = 0;
+    void* hX[kSlots] = {};  // pinned staging for pageable callers (allocated on first use)
+    void* hY[kSlots] = {};
+    size_t hxcap = 0, hycap = 0;
+    CopyPool pool;
 
     cudaError_t init(int dev) {
         if (in) return cudaSuccess;
@@ -91,6 +247,31 @@ struct HostPipeline {
         ycap = yb;
         return cudaSuccess;
     }
+    // Pinned host staging slots of at least xb / yb bytes (pageable callers).
+    cudaError_t reserve_pinned(size_t xb, size_t yb) {
+        if (xb <= hxcap && yb <= hycap) return cudaSuccess;
+        release_pinned();
+        cudaError_t e = cudaSuccess;
+        for (int i = 0; i < kSlots && e == cudaSuccess; ++i) {
+            e = cudaHostAlloc(&hX[i], xb, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaHostAlloc(&hY[i], yb, cudaHostAllocDefault);
+        }
+        if (e != cudaSuccess) {
+            release_pinned();
+            return e;
+        }
+        hxcap = xb;
+        hycap = yb;
+        return cudaSuccess;
+    }
+    void release_pinned() {
+        for (int i = 0; i < kSlots; ++i) {
+            if (hX[i]) cudaFreeHost(hX[i]);
+            if (hY[i]) cudaFreeHost(hY[i]);
+            hX[i] = hY[i] = nullptr;
+        }
+        hxcap = hycap = 0;
+    }
     void release() {
         for (int i = 0; i < kSlots; ++i) {
             if (dX[i]) cudaFree(dX[i]);
@@ -101,6 +282,7 @@ struct HostPipeline {
     }
     void destroy() {
         release();
+        release_pinned();
         for (int i = 0; i < kSlots; ++i)
             for (cudaEvent_t* ev : {&h2d[i], &kdone[i], &d2h[i]}) {
                 if (*ev) cudaEventDestroy(*ev);
@@ -121,11 +303,16 @@ struct HostPipeline {
 //   compute(c, dX, dY, stream) - enqueue the chunk's kernels; returns a status
 // Blocks until every chunk's D2H has landed. Returns the first failing status
 // (`cuda_fail(e, what)` maps CUDA errors).
+//
+// widen_out: the device result is fp32 while the caller's Y is fp64 (dst gives
+// the fp64 buffer and its byte count): the D2H moves the fp32 bytes (half) into
+// a pinned slot and the host pool widens them into Y.
 template <class Src, class Dst, class Compute, class Fail>
-int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute compute, Fail cuda_fail) {
+int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute compute, Fail cuda_fail,
+                      bool widen_out = false) {
     constexpr int S = HostPipeline::kSlots;
     int rc = 0;
-    if (chunks == 1) {  // nothing to overlap: one stream, no cross-stream events (small batches)
+    if (chunks == 1 && !widen_out) {  // nothing to overlap: one stream, no cross-stream events (small batches)
         const void* hs = nullptr;
         void* hd = nullptr;
         size_t xb = 0, yb = 0;
@@ -142,6 +329,42 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         return e == cudaSuccess ? 0 : cuda_fail(e, "host pipeline: D2H");
     }
+    // pageable caller buffers go through the pinned slots (see the header comment)
+    const void* hs0 = nullptr;
+    void* hd0 = nullptr;
+    size_t xb0 = 0, yb0 = 0;
+    src(0, &hs0, &xb0);
+    dst(0, &hd0, &yb0);
+    const bool stage_in = is_pageable(hs0), stage_out = widen_out || is_pageable(hd0);
+    const size_t yscale = widen_out ? 2 : 1;  // host Y bytes per device Y byte
+    if (stage_in || stage_out) {
+        size_t xmax = 0, ymax = 0;
+        for (int64_t c = 0; c < chunks; ++c) {
+            const void* a = nullptr;
+            void* d = nullptr;
+            size_t xb = 0, yb = 0;
+            src(c, &a, &xb);
+            dst(c, &d, &yb);
+            xmax = std::max(xmax, xb);
+            ymax = std::max(ymax, yb);
+        }
+        const cudaError_t e = P.reserve_pinned(stage_in ? xmax : 0, stage_out ? ymax / yscale : 0);
+        if (e != cudaSuccess) return cuda_fail(e, "host pipeline: pinned staging");
+    }
+    // copy chunk c's result out of its pinned slot into the caller's buffer
+    auto drain = [&](int64_t c) -> int {
+        if (!stage_out || c < 0) return 0;
+        void* hd = nullptr;
+        size_t yb = 0;
+        dst(c, &hd, &yb);
+        const cudaError_t e = cudaEventSynchronize(P.d2h[c % S]);
+        if (e != cudaSuccess) return cuda_fail(e, "host pipeline: D2H");
+        if (widen_out)
+            P.pool.widen(static_cast<double*>(hd), static_cast<const float*>(P.hY[c % S]), yb / sizeof(double));
+        else
+            P.pool.copy(hd, P.hY[c % S], yb);
+        return 0;
+    };
     for (int64_t c = 0; c < chunks && rc == 0; ++c) {
         const int b = static_cast<int>(c % S);
         const void* hs = nullptr;
@@ -150,6 +373,16 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
         src(c, &hs, &xb);
         dst(c, &hd, &yb);
         cudaError_t e = cudaSuccess;
+        if (stage_in) {  // the slot's previous H2D (chunk c - S) has finished reading it
+            if (c >= S) e = cudaEventSynchronize(P.h2d[b]);
+            if (e != cudaSuccess) {
+                rc = cuda_fail(e, "host pipeline: H2D");
+                break;
+            }
+            P.pool.copy(P.hX[b], hs, xb);
+            hs = P.hX[b];
+        }
+        if (stage_out) hd = P.hY[b];  // chunk c - S was drained from it at iteration c - 1
         if (c >= S) e = cudaStreamWaitEvent(P.in, P.kdone[b], 0);  // chunk c - S has consumed dX[b]
         if (e == cudaSuccess) e = cudaMemcpyAsync(P.dX[b], hs, xb, cudaMemcpyHostToDevice, P.in);
         if (e == cudaSuccess) e = cudaEventRecord(P.h2d[b], P.in);
@@ -164,10 +397,15 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
         if (rc) break;
         e = cudaEventRecord(P.kdone[b], comp);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(P.out, P.kdone[b], 0);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hd, P.dY[b], yb, cudaMemcpyDeviceToHost, P.out);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hd, P.dY[b], yb / yscale, cudaMemcpyDeviceToHost, P.out);
         if (e == cudaSuccess) e = cudaEventRecord(P.d2h[b], P.out);
         if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline: D2H");
+        // drain two chunks behind, so the GPU always has chunks c-1 and c queued
+        // while the host copies (slot c % S's Y was drained at iteration c - 1)
+        if (rc == 0) rc = drain(c - 2);
     }
+    if (rc == 0) rc = drain(chunks - 2);
+    if (rc == 0) rc = drain(chunks - 1);
     for (cudaStream_t s : {P.in, P.comp[0], P.comp[1], P.out}) {
         const cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess && rc == 0) rc = cuda_fail(e, "host pipeline: stream sync");

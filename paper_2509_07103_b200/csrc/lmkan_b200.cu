@@ -612,7 +612,13 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     const int64_t nchunks = std::max(1, env_int("LMKAN_B200_HOST_CHUNKS", 8));
     int64_t chunk = std::max<int64_t>({(rows + nchunks - 1) / nchunks, min_chunk, 1});
     chunk = std::min(chunk, rows);
-    CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT), static_cast<size_t>(chunk) * L->n_out * sizeof(XT)));
+    // fp64 callers: Y crosses PCIe as fp32 (exact: every output is an fp32 sum
+    // times an fp32 gamma) and is widened on the host; the slot's device Y holds
+    // [fp32 Y | fp64 Y]
+    const bool widen = sizeof(XT) == 8 && env_int("LMKAN_B200_HOST_F32_Y", 1) != 0;
+    const size_t y32_bytes = (static_cast<size_t>(chunk) * L->n_out * sizeof(float) + 255) & ~static_cast<size_t>(255);
+    CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT),
+                 static_cast<size_t>(chunk) * L->n_out * sizeof(XT) + (widen ? y32_bytes : 0)));
     const ChunkSchedule cs(rows, chunk, env_int("LMKAN_B200_HOST_TAPER", 1) != 0);  // cfg2 e2e 3.51e6 -> 3.58e6
     return run_host_pipeline(
         P, cs.count(),
@@ -625,9 +631,17 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
             *b = static_cast<size_t>(cs.size(c)) * L->n_out * sizeof(XT);
         },
         [&](int64_t c, void* dX, void* dY, cudaStream_t st) {
-            return forward_device<XT>(L, static_cast<const XT*>(dX), static_cast<XT*>(dY), cs.size(c), st);
+            if (!widen)
+                return forward_device<XT>(L, static_cast<const XT*>(dX), static_cast<XT*>(dY), cs.size(c), st);
+            XT* y64 = reinterpret_cast<XT*>(static_cast<char*>(dY) + y32_bytes);
+            if (int rc = forward_device<XT>(L, static_cast<const XT*>(dX), y64, cs.size(c), st)) return rc;
+            const size_t n = static_cast<size_t>(cs.size(c)) * L->n_out;
+            narrow_f64_kernel<<<fill_blocks(n), 256, 0, st>>>(reinterpret_cast<const double*>(y64),
+                                                              static_cast<float*>(dY), n);
+            const cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? LMKAN_B200_OK : cuda_fail(e, "lmkan_forward: narrow Y");
         },
-        [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
+        [](cudaError_t e, const char* what) { return cuda_fail(e, what); }, widen);
 }
 
 }  // namespace

@@ -85,4 +85,12 @@ static __global__ void export_kernel(const float* __restrict__ table, double* __
     }
 }
 
+// fp64 results that are exactly fp32 values (the gather accumulates in fp32)
+// narrowed for a half-size D2H (host paths with fp64 Y; widened back on the host).
+static __global__ void narrow_f64_kernel(const double* __restrict__ src, float* __restrict__ dst, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dst[i] = static_cast<float>(src[i]);
+}
+
 }  // namespace lmkan_b200

@@ -169,6 +169,38 @@ static void test_determinism_and_cache() {  // test_layer.cpp:228-239 + P edits
     layer.gamma = 0.0;
     lmkan_forward(layer, X, Y2);
     for (std::size_t i = 0; i < Y2.size(); ++i) CHECK(Y2.data()[i] == 0.0);
+    layer.gamma = 0.9;
+    // every mutation route of P (a ParamVector) is seen by the next forward:
+    // element reference, data() pointer (taken after the last forward, as the
+    // reference's optimizer does, model.hpp:382-386), a std::vector<double>&
+    // parameter, assign(), whole assignment; a const read is not a mutation
+    auto scale_via = [&](int how, double f) {
+        switch (how) {
+            case 0: for (std::size_t i = 0; i < layer.P.size(); ++i) layer.P[i] *= f; break;
+            case 1: { double* p = layer.P.data(); for (std::size_t i = 0; i < layer.P.size(); ++i) p[i] *= f; } break;
+            case 2: { auto mul = [f](std::vector<double>& v) { for (double& x : v) x *= f; }; mul(layer.P); } break;
+            case 3: { std::vector<double> v(layer.P.begin(), layer.P.end()); for (double& x : v) x *= f;
+                      layer.P.assign(v.begin(), v.end()); } break;
+            default: { std::vector<double> v = layer.P; for (double& x : v) x *= f; layer.P = v; } break;
+        }
+    };
+    Matrix Yref;
+    lmkan_forward(layer, X, Yref);
+    for (int how = 0; how < 5; ++how) {
+        const std::uint64_t g0 = layer.P.generation();
+        const LmKanLayer& cl = layer;
+        double sum = 0.0;
+        for (std::size_t i = 0; i < cl.P.size(); ++i) sum += cl.P[i];  // const reads
+        CHECK(layer.P.generation() == g0 && std::isfinite(sum));
+        scale_via(how, -1.0);
+        CHECK(layer.P.generation() != g0);
+        Matrix Ys;
+        lmkan_forward(layer, X, Ys);
+        for (std::size_t i = 0; i < Ys.size(); ++i) CHECK(Ys.data()[i] == -Yref.data()[i]);
+        scale_via(how, -1.0);
+        lmkan_forward(layer, X, Ys);
+        for (std::size_t i = 0; i < Ys.size(); ++i) CHECK(Ys.data()[i] == Yref.data()[i]);
+    }
 }
 
 static void test_grid_helpers() {  // test_grid.cpp:34-48, 166-219 restated

@@ -582,3 +582,24 @@ def test_output_slices_across_table_layouts_bitwise(torch, pkg):
         sl = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0, out_range=(ob, oe))
         assert torch.equal(sl.forward(X), Y[:, ob:oe]), (ob, oe, sl.out_tile)
         np.testing.assert_array_equal(sl.read_table(), P[..., ob:oe].astype(np.float64))
+
+
+@pytest.mark.parametrize("x_pinned,y_pinned", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_host_staging_paths_bitwise(torch, pkg, monkeypatch, x_pinned, y_pinned, dtype):
+    """Host entry points with pageable and/or pinned caller buffers: pageable
+    ones are staged through pinned slots by the copy pool (non-temporal copies,
+    fp64 Y crossing PCIe as fp32 and widened on the host). Every combination
+    equals the device path bitwise, over several chunks with a ragged tail."""
+    monkeypatch.setenv("LMKAN_B200_HOST_CHUNKS", "5")
+    layer = pkg.Layer.random(96, 80, 12, seed=33)
+    rows = 70001
+    tdt = getattr(torch, dtype)
+    Xd = (torch.randn((rows, 96), device="cuda", dtype=torch.float64) * 1.3).to(tdt)
+    want = layer.forward(Xd).cpu().numpy()
+    Xh = Xd.cpu().pin_memory() if x_pinned else Xd.cpu()
+    Yh = torch.empty((rows, 80), dtype=tdt).pin_memory() if y_pinned else torch.empty((rows, 80), dtype=tdt)
+    Yh.fill_(float("nan"))
+    layer.forward_host_ptr(Xh.data_ptr(), Yh.data_ptr(), rows, np.dtype(dtype).type)
+    assert np.array_equal(Yh.numpy(), want)
+    assert np.array_equal(layer.forward_host(Xh.numpy()), want)
