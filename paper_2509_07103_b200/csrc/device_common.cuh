@@ -30,6 +30,7 @@ struct InputMap {
     int conv;  // 0: dense X, 1: implicit im2col over an NHWC image batch
     int out_h, out_w, H, W, C, k, s;
     int64_t row_offset;
+    int64_t npix;  // conv: pixels of the image batch, N*H*W (pixel-record stride, kModePixel)
 };
 __host__ __device__ inline int64_t in_rowbase(const InputMap& m, int64_t r, int n_in) {
     r += m.row_offset;

@@ -12,6 +12,8 @@ enum : int {
     kModeStaged = 1,  // K2: cell records produced by K1 (records_kernel), sheets + records via bulk copy
     kModeGlobal = 2,  // fallback for sheets larger than shared memory: in-kernel locate, sheets read from L2
     kModeNarrow = 3,  // K4: n_out <= 4, whole table resident in shared memory, lanes over pairs
+    kModePixel = 4,   // K3 for the implicit-im2col conv: records located once per image pixel
+                      // (pixel_records_kernel) and fetched per (row, pair) through the im2col map
 };
 
 // Float4 runs of outputs per lane. At OT = 64 a lane covers 16 outputs (four
@@ -360,6 +362,37 @@ __global__ void __launch_bounds__(256) locate_ag_kernel(const XT* __restrict__ X
     }
 }
 
+// Pixel records for the implicit-im2col conv (kModePixel): the cell of a
+// channel pair depends only on the input pixel, and a k x k conv reads every
+// pixel in k^2 patch rows, so locating per pixel instead of per (row, pair)
+// does 1/k^2 of the work. out[cp][pixel] = {alpha, gamma, packed offset, 0}
+// for channel pair cp = (2cp, 2cp+1) of every pixel of the NHWC batch
+// (npix = N*H*W), computed exactly as the in-kernel locate would (locate_ag,
+// same node stride NS and slab height H). Thread per (cp, pixel), pixel
+// fastest: coalesced record stores.
+template <typename XT>
+__global__ void __launch_bounds__(256) pixel_records_kernel(const XT* __restrict__ img, int64_t npix, int C,
+                                                            const __grid_constant__ GridConst gc, int NS, int H,
+                                                            int4* __restrict__ out) {
+    __shared__ XT thr[kMaxThr];
+    __shared__ double pts[kMaxThr + 1];
+    __shared__ double invh[kMaxThr];
+    const int G = gc.G;
+    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = threadIdx.x; k <= G; k += blockDim.x) pts[k] = gc.points[k];
+    for (int k = threadIdx.x; k < G; k += blockDim.x) invh[k] = gc.inv_h[k];
+    __syncthreads();
+    const int64_t total = npix * (C / 2);
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t cp = k / npix, pix = k - cp * npix;
+        const XT* x = img + pix * C + 2 * cp;
+        float2 ag;
+        const int packed = locate_ag<XT>(x[0], x[1], thr, pts, invh, G, gc.L, NS, H, ag);
+        out[k] = make_int4(__float_as_int(ag.x), __float_as_int(ag.y), packed, 0);
+    }
+}
+
 // K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
 // Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
 // [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of
@@ -445,7 +478,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const uint32_t recw_copy = static_cast<uint32_t>(Rt) * 8u;  // this tile's records (<= L.recw_bytes)
     const int units = pairs * S;
 
-    if constexpr (MODE != kModeStaged) {
+    constexpr bool kLocate = MODE == kModeFused || MODE == kModeGlobal;  // in-kernel locate
+    constexpr bool kPix = MODE == kModePixel;
+    if constexpr (kLocate) {
         for (int k = tid; k < kMaxThr; k += NT) thr[k] = thr_of<XT>(gc)[k];
         for (int k = tid; k <= G; k += NT) pts[k] = gc.points[k];
         for (int k = tid; k < G; k += NT) inv[k] = gc.inv_h[k];
@@ -497,9 +532,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     }
 
-    // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane
+    // --- warp-local cell locate (fused / global): lane handles rows q = k*32 + lane;
+    // pixel mode: the lane fetches those rows' records of the pixel each pair reads
     XT xa[Sh::LOC], xb[Sh::LOC];
     const XT* xrow[Sh::LOC];
+    int pixb[Sh::LOC];     // pixel mode: the row's top-left input pixel (absolute index)
+    int4 prec[Sh::LOC];    // pixel mode: the prefetched records {alpha, gamma, packed offset, 0}
+    const int4* const pixrec = reinterpret_cast<const int4*>(recO);
     // float2 x-pair loads when both columns are adjacent and 8-byte aligned
     const bool x_vec_ok = (reinterpret_cast<uintptr_t>(X) & 7) == 0 && (!im.conv || (im.C & 1) == 0);
 #pragma unroll
@@ -508,8 +547,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int64_t r = row0 + warp * Sh::ROWS_W + q;
         const bool in_tile = warp * Sh::ROWS_W + q < Rt;
         xrow[k] = (MODE != kModeStaged && q < Sh::ROWS_W && in_tile && r < rows) ? X + in_rowbase(im, r, n_in) : nullptr;
+        if constexpr (kPix) pixb[k] = xrow[k] ? static_cast<int>(in_rowbase(im, r, n_in) / im.C) : 0;
     }
     auto prefetch = [&](int p) {
+        if constexpr (kPix) {  // pair p = channels (ch, ch+1) of tap (dy, dx): record [ch/2][pixel + tap offset]
+            const int tap = (2 * p) / im.C, ch = 2 * p - tap * im.C;
+            const int dy = tap / im.k, dx = tap - dy * im.k;
+            const int4* base = pixrec + static_cast<int64_t>(ch >> 1) * im.npix + dy * im.W + dx;
+#pragma unroll
+            for (int k = 0; k < Sh::LOC; ++k) prec[k] = xrow[k] ? __ldg(base + pixb[k]) : make_int4(0, 0, 0, 0);
+            return;
+        }
         const int c0 = in_coloff(im, 2 * p), c1 = im.conv ? in_coloff(im, 2 * p + 1) : c0 + 1;
 #pragma unroll
         for (int k = 0; k < Sh::LOC; ++k) {
@@ -535,7 +583,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (q < Sh::ROWS_W) {
                 float2 ag = make_float2(0.f, 0.f);
                 int packed = 0;
-                if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, NS, H, ag);
+                if constexpr (kPix) {
+                    ag = make_float2(__int_as_float(prec[k].x), __int_as_float(prec[k].y));
+                    packed = prec[k].z;
+                } else {
+                    if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, NS, H, ag);
+                }
                 const int qc = warp * Sh::ROWS_W + q;
                 rec_w[qc] = ag;
                 rec_o[offset_slot(shp, qc)] = packed;

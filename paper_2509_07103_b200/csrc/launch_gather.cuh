@@ -72,10 +72,14 @@ cudaError_t launch_gather(const lmkan_b200_layer* L, const Plan& pl, const XT* X
                            const GridConst* gc_next, cudaStream_t st) {
     if constexpr (DUP) {  // duplicated-node tables: unslabbed shared-memory sheets only (planner)
         if (pl.mode == kModeGlobal || pl.S > 1) return cudaErrorInvalidConfiguration;
+        if (pl.mode == kModeFused && pl.pix)
+            return launch_fused_rt<OT, XT, kModePixel, false, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
         return pl.mode == kModeStaged
                    ? launch_fused_rt<OT, XT, kModeStaged, false, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st)
                    : launch_fused_rt<OT, XT, kModeFused, false, true>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
     } else {
+        if (pl.mode == kModeFused && pl.pix && pl.S == 1)
+            return launch_fused_rt<OT, XT, kModePixel, false>(L, pl, X, Y, rows, recW, recO, im, emit, gc_next, st);
         if (pl.mode == kModeGlobal)
             return launch_fused_t<OT, 4 / lane_vectors(OT), XT, kModeGlobal, false>(L, pl, X, Y, rows, recW, recO, im,
                                                                                    emit, gc_next, st);

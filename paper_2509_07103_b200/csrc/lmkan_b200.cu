@@ -352,21 +352,40 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
             return cuda_fail(e, "lmkan_forward: records kernel launch");
         }
     }
+    // implicit-im2col conv in the fused mode: locate once per image pixel
+    // (pixel_records_kernel, 1/k^2 of the per-(row, pair) locates) and let the
+    // gather fetch the records through the im2col map (kModePixel)
+    Plan plx = pl;
+    int4* pixrec = nullptr;
+    if (pl.mode == kModeFused && pl.S == 1 && im.conv && im.C % 2 == 0 && im.npix > 0 &&
+        im.npix < (int64_t(1) << 31) && !link.emit.W && env_int("LMKAN_B200_PIXREC", 1)) {
+        const int64_t nrec = im.npix * (im.C / 2);
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&pixrec), static_cast<size_t>(nrec) * sizeof(int4), st));
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((nrec + 255) / 256, kNumSMs * 16));
+        pixel_records_kernel<XT><<<blocks, 256, 0, st>>>(X, im.npix, im.C, L->gc, L->ns, L->G, pixrec);
+        const cudaError_t e1 = cudaGetLastError();
+        if (e1 != cudaSuccess) {
+            cudaFreeAsync(pixrec, st);
+            return cuda_fail(e1, "lmkan_forward: pixel records kernel launch");
+        }
+        plx.pix = 1;
+        recO = reinterpret_cast<int*>(pixrec);
+    }
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
     const float2* useW = link.preW ? link.preW : recW;
     const int* useO = link.preW ? link.preO : recO;
     switch (L->OT) {
-        case 64: e = launch_gather<64, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
-        case 32: e = launch_gather<32, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
+        case 64: e = launch_gather<64, XT>(L, plx, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
+        case 32: e = launch_gather<32, XT>(L, plx, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st); break;
         default:
-            e = L->dup ? launch_gather<16, XT, true>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st)
-                       : launch_gather<16, XT>(L, pl, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st);
+            e = L->dup ? launch_gather<16, XT, true>(L, plx, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st)
+                       : launch_gather<16, XT>(L, plx, X, Y, rows, useW, useO, im, link.emit, link.gc_next, st);
             break;
     }
     if (ev_end) cudaEventRecord(ev_end, st);
     if (recW) cudaFreeAsync(recW, st);
-    if (recO) cudaFreeAsync(recO, st);
+    if (recO) cudaFreeAsync(recO, st);  // K1 records or the pixel records
     if (e != cudaSuccess) return cuda_fail(e, "lmkan_forward: gather kernel launch");
     return LMKAN_B200_OK;
 }
@@ -566,6 +585,12 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // no hidden cross-stream waits: with internal-dependency reuse an
+            // allocation on one compute stream of the host pipeline may wait on a
+            // free enqueued on the other, serialising the two streams
+            // (LMKAN_B200_POOL_DEPS=1 restores the default for A/B runs)
+            int deps = env_int("LMKAN_B200_POOL_DEPS", 0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &deps);
         }
     }
     *out = L;
@@ -928,6 +953,7 @@ int conv_map(const lmkan_b200_layer* L, int N, int H, int W, int C, int k, int s
     im.C = C;
     im.k = k;
     im.s = s;
+    im.npix = static_cast<int64_t>(N) * H * W;
     return LMKAN_B200_OK;
 }
 }  // namespace
@@ -967,8 +993,10 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
             *b = sizeof(float) * out_img * cs.size(c);
         },
         [&](int64_t c, void* dI, void* dY, cudaStream_t st) {
+            InputMap imc = im;
+            imc.npix = static_cast<int64_t>(cs.size(c)) * H * W;  // the chunk's images only
             return forward_device<float>(L, static_cast<const float*>(dI), static_cast<float*>(dY),
-                                         per_img * cs.size(c), st, nullptr, nullptr, im);
+                                         per_img * cs.size(c), st, nullptr, nullptr, imc);
         },
         [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
 }

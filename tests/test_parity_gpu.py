@@ -393,6 +393,9 @@ def _unfold(img, k, s):
     (3, 8, 8, 6, 2, 2, 40, 5),
     (2, 7, 9, 3, 2, 1, 10, 6),       # odd C: x pairs straddle taps
     (2, 6, 6, 4, 3, 1, 2, 12),       # narrow head (n_out <= 4)
+    (3, 18, 18, 32, 3, 1, 32, 16),   # CIFAR stage-2 geometry (OT 32)
+    (2, 10, 10, 64, 3, 1, 64, 16),   # CIFAR stage-3 geometry (OT 64)
+    (2, 11, 13, 8, 3, 2, 24, 9),     # stride 2, non-square
 ])
 def test_conv_implicit_im2col(torch, pkg, oracle, N, H, W, C, k, s, n_out, G):
     rng = np.random.default_rng(N * 100 + C)
@@ -419,6 +422,20 @@ def test_conv_host_chunked_cfg4_shape(torch, pkg):
     layer = pkg.Layer.random(144, 16, 16, seed=4)
     Yd = layer.conv_forward(torch.from_numpy(img).cuda(), 3, 1).cpu().numpy()
     assert np.array_equal(layer.conv_forward_host(img, 3, 1), Yd)
+
+
+@pytest.mark.parametrize("N,H,W,C,n_out,G", [(40, 34, 34, 16, 16, 16), (20, 18, 18, 32, 32, 16),
+                                             (10, 10, 10, 64, 64, 16), (6, 9, 9, 6, 20, 28)])
+def test_conv_pixel_records_bitwise(torch, pkg, monkeypatch, N, H, W, C, n_out, G):
+    """Records located once per image pixel (pixel_records_kernel, kModePixel)
+    give the same output bits as the per-(row, pair) in-kernel locate."""
+    rng = np.random.default_rng(C + N)
+    img = torch.from_numpy(rng.standard_normal((N, H, W, C)).astype(np.float32) * 1.4).cuda()
+    layer = pkg.Layer.random(9 * C, n_out, G, seed=C)
+    Y = layer.conv_forward(img, 3, 1)
+    monkeypatch.setenv("LMKAN_B200_PIXREC", "0")
+    Y0 = layer.conv_forward(img, 3, 1)
+    assert torch.equal(Y, Y0)
 
 
 def test_conv_argument_errors(torch, pkg):
