@@ -602,6 +602,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[j][v] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int rstride = (G + 1) * NS;  // node (i1+1, i2) is (G+1) nodes further
+    // conflict-free loads of plain (not duplicated) OT = 16 sheets by bank-half
+    // swapping (see the gather loop); LMKAN_B200_HALFSWAP=0 builds without
+#ifndef LMKAN_B200_HALFSWAP
+#define LMKAN_B200_HALFSWAP 1
+#endif
+    constexpr bool kHalfSwap = LMKAN_B200_HALFSWAP && OT == 16 && !DUP && V == 1 && kSmemSheet;
+    const bool gpar = ((G + 1) & 1) != 0;  // rows i1 and i1 + 1 of a node pair on opposite halves
     // The planner makes Rt a multiple of ROWS_W, so a warp's rows are all inside
     // the tile or all beyond it: warps beyond it issue no gathers. Rows past the
     // batch end inside the last tile gather zero-weight records (no branch in
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 const int rs = MODE == kModeStaged ? p % L.nrec : 0;
                 rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
                 if constexpr (GOFF) {
-    #pragma unroll
+#pragma unroll
                     for (int j = 0; j < RT; ++j) offs[j] = offs_next[j];
                     if (p + 1 < pairs) load_offs(offs_src(p + 1), offs_next, true);
                 } else {
@@ -722,7 +729,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 }
             }
             if (!TAIL || warp_live) {  // TAIL: shortened row tiles, some warps hold no rows
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < RT; ++j) {
                     if constexpr (SLAB) {
                         // rows whose cell lies in another slab load nothing and add +0
@@ -730,7 +737,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         const float* b0 = sh + (offs[j] & kOffMask);
                         const float* b1 = b0 + rstride;
                         const float4 w = weights_ag(lds64_if(rw + j * Sh::RPW, ok));
-    #pragma unroll
+#pragma unroll
                         for (int v = 0; v < V; ++v) {
                             const float4 p00 = lds128_if(b0 + vofs(v), ok);
                             const float4 p01 = lds128_if(b0 + vofs(v) + NS, ok);
@@ -742,10 +749,27 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         const float4 w = weights_ag(rw[j * Sh::RPW]);
                         const float* b0 = sh + offs[j];
                         const float* b1 = b0 + rstride;
-    #pragma unroll
+#pragma unroll
                         for (int v = 0; v < V; ++v) {
                             float4 p00, p01, p10, p11;
-                            if constexpr (kSmemSheet) {
+                            if constexpr (kHalfSwap) {
+                                // plain OT = 16 sheet: node n's 64-B run sits on bank half
+                                // (address / 64) & 1, n + 1 on the other. Each lane group
+                                // loads first the member of {n, n+1} (and of
+                                // {n+G+1, n+G+2}) on ITS half (sub & 1), so every LDS puts
+                                // 4 rows on each half (4 wavefronts, no conflicts), then
+                                // un-swaps in registers: the FMA order stays p00, p10, p01, p11.
+                                const bool sw0 = ((smem_addr(b0) >> 6) & 1u) != static_cast<uint32_t>(sub & 1);
+                                const bool sw1 = sw0 != gpar;
+                                const float4 r0 = *reinterpret_cast<const float4*>(sw0 ? b0 + NS : b0);
+                                const float4 r1 = *reinterpret_cast<const float4*>(sw1 ? b1 + NS : b1);
+                                const float4 r2 = *reinterpret_cast<const float4*>(sw0 ? b0 : b0 + NS);
+                                const float4 r3 = *reinterpret_cast<const float4*>(sw1 ? b1 : b1 + NS);
+                                p00 = sw0 ? r2 : r0;
+                                p01 = sw0 ? r0 : r2;
+                                p10 = sw1 ? r3 : r1;
+                                p11 = sw1 ? r1 : r3;
+                            } else if constexpr (kSmemSheet) {
                                 p00 = *reinterpret_cast<const float4*>(b0 + vofs(v));
                                 p01 = *reinterpret_cast<const float4*>(b0 + vofs(v) + NS);
                                 p10 = *reinterpret_cast<const float4*>(b1 + vofs(v));
