@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                                 p10 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v)));
                                 p11 = __ldg(reinterpret_cast<const float4*>(b1 + vofs(v) + NS));
                             }
-                            fma_corners(acc[j][v], w, p00, p10, p01, p11);
+                            fma_corners<kHalfSwap>(acc[j][v], w, p00, p10, p01, p11);
                         }
                     }
                 }

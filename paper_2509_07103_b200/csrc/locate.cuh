@@ -144,8 +144,33 @@ __device__ __forceinline__ float4 weights_ag(float2 ag) {
 
 // acc += ((w00 p00 + w10 p10) + w01 p01) + w11 p11 per output, fused
 // multiply-adds in the reference's per-pair grouping (layer.hpp:129).
+// PACKED: two outputs per instruction on the packed fp32x2 pipe (FMUL2 /
+// FFMA2 / FADD2, sm_100). Every lane of a packed op is the same IEEE
+// round-to-nearest operation, so the results are bit-identical to the scalar
+// form at half the FP instruction count. It pays only where issue slots bind:
+// the bank-half-swapped OT = 16 gather (config 5 shard 744 -> 698 ms); on the
+// latency-bound gathers it measured slower (config 3 chain 5.86 -> 6.08 ms,
+// config 2 +0.5%), so they keep the scalar form.
+template <bool PACKED = false>
 __device__ __forceinline__ void fma_corners(float4& acc, const float4 w, const float4 p00, const float4 p10,
                                             const float4 p01, const float4 p11) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    if constexpr (PACKED) {
+        const float2 w0 = make_float2(w.x, w.x), w1 = make_float2(w.y, w.y), w2 = make_float2(w.z, w.z),
+                     w3 = make_float2(w.w, w.w);
+        const float2 lo = __ffma2_rn(w3, make_float2(p11.x, p11.y),
+                                     __ffma2_rn(w2, make_float2(p01.x, p01.y),
+                                                __ffma2_rn(w1, make_float2(p10.x, p10.y),
+                                                           __fmul2_rn(w0, make_float2(p00.x, p00.y)))));
+        const float2 hi = __ffma2_rn(w3, make_float2(p11.z, p11.w),
+                                     __ffma2_rn(w2, make_float2(p01.z, p01.w),
+                                                __ffma2_rn(w1, make_float2(p10.z, p10.w),
+                                                           __fmul2_rn(w0, make_float2(p00.z, p00.w)))));
+        const float2 a = __fadd2_rn(make_float2(acc.x, acc.y), lo), b = __fadd2_rn(make_float2(acc.z, acc.w), hi);
+        acc = make_float4(a.x, a.y, b.x, b.y);
+        return;
+    }
+#endif
     acc.x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
     acc.y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
     acc.z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
