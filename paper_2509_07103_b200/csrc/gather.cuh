@@ -122,7 +122,9 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
     const int nb = nbuf > 0 ? nbuf : 1;
     FusedSmem s;
     s.nrec = mode == kModeStaged ? staged_nrec(nb, S) : 1;
-    s.sheet_bytes = static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * (NS > 0 ? NS : OT) * 4u;
+    // slot stride rounded to 128 B: node n's 64-B run of a plain OT = 16 sheet
+    // then sits on bank half n & 1 in every slot (bank-half swap, locate_ag)
+    s.sheet_bytes = (static_cast<uint32_t>(slab_node_rows(G, H, 0)) * (G + 1) * (NS > 0 ? NS : OT) * 4u + 127u) & ~127u;
     s.recw_bytes = sh.R * 8u;  // float2 {alpha, gamma} per row
     // goff (staged only): node offsets go global -> registers (prefetched a pair
     // ahead) instead of riding the ring with the records, so the ring holds only
@@ -168,7 +170,7 @@ template <typename XT, bool SHORT_TILES>
 __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                       int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
                                                       int H, float2* __restrict__ W, int* __restrict__ O,
-                                                      const InputMap im, int64_t Rt) {
+                                                      const InputMap im, int64_t Rt, int hs) {
     __shared__ XT xs[64][33];
     __shared__ int64_t rbase[64];
     __shared__ int coff[32];
@@ -228,7 +230,8 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
                     float2 ag = make_float2(0.f, 0.f);
                     int packed = 0;
                     if (g < rows)
-                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag);
+                        packed = locate_ag<XT>(xs[r][2 * pl], xs[r][2 * pl + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag,
+                                               hs ? static_cast<int>((g - tile * Rt) & 1) : -1);
                     *wp = ag;
                     *op = packed;
                 }
@@ -249,7 +252,7 @@ template <typename XT, bool SHORT_TILES>
 __global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X, int64_t rows, int64_t rows_pad,
                                                        int n_in, const __grid_constant__ GridConst gc, ShapeRT sh,
                                                        int H, float2* __restrict__ W, int* __restrict__ O,
-                                                       const InputMap im, int64_t Rt, int vec) {
+                                                       const InputMap im, int64_t Rt, int vec, int hs) {
     __shared__ XT thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
     __shared__ double invh[kMaxThr];
@@ -289,7 +292,9 @@ __global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X,
             if (k < np) {
                 float2 ag = make_float2(0.f, 0.f);
                 int packed = 0;
-                if (g < rows) packed = locate_ag<XT>(x[2 * k], x[2 * k + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag);
+                if (g < rows)
+                    packed = locate_ag<XT>(x[2 * k], x[2 * k + 1], thr, pts, invh, G, gc.L, sh.NS, H, ag,
+                                           hs ? static_cast<int>((g - tile * Rt) & 1) : -1);
                 wp[k * wstep] = ag;
                 op[k * ostep] = packed;
             }
@@ -302,8 +307,9 @@ __global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X,
 // (layer.hpp:96-101): per (row, pair) the cell (i1, i2) and {alpha, gamma}.
 // Packed offset = (slab << 24) | (node-within-slab * NS), node = i1'(G+1) + i2.
 __device__ __forceinline__ void decode_packed(int packed, int G, int H, int NS, int& i1, int& i2) {
-    const int s = packed >> kSlabShift;
-    const int nodews = (packed & kOffMask) / NS;
+    const int sw = (packed >> kSwapBit) & 1;  // bank-half-swapped record: offset names node n + 1
+    const int s = (packed >> kSlabShift) & 0x3f;
+    const int nodews = (packed & kOffMask) / NS - sw;
     i1 = s * H + nodews / (G + 1);
     i2 = nodews % (G + 1);
 }
@@ -335,7 +341,7 @@ static __global__ void __launch_bounds__(256) decode_records_kernel(const float2
 // slab height H), one thread per (row, pair), decoded like decode_records_kernel.
 template <typename XT>
 __global__ void __launch_bounds__(256) locate_ag_kernel(const XT* __restrict__ X, int64_t rows, int n_in,
-                                                        const __grid_constant__ GridConst gc, int NS, int H,
+                                                        const __grid_constant__ GridConst gc, int NS, int H, int hs,
                                                         int32_t* __restrict__ o_i1, int32_t* __restrict__ o_i2,
                                                         float2* __restrict__ o_ag) {
     __shared__ XT thr[kMaxThr];
@@ -355,7 +361,8 @@ __global__ void __launch_bounds__(256) locate_ag_kernel(const XT* __restrict__ X
         const XT* xr = X + r * n_in + 2 * p;
         float2 ag;
         int i1, i2;
-        decode_packed(locate_ag<XT>(xr[0], xr[1], thr, pts, invh, G, gc.L, NS, H, ag), G, H, NS, i1, i2);
+        decode_packed(locate_ag<XT>(xr[0], xr[1], thr, pts, invh, G, gc.L, NS, H, ag, hs ? static_cast<int>(r & 1) : -1),
+                      G, H, NS, i1, i2);
         o_i1[k] = i1;
         o_i2[k] = i2;
         o_ag[k] = ag;
@@ -478,6 +485,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const uint32_t recw_copy = static_cast<uint32_t>(Rt) * 8u;  // this tile's records (<= L.recw_bytes)
     const int units = pairs * S;
 
+    // conflict-free loads of plain (not duplicated) OT = 16 sheets by bank-half
+    // swapped records (locate_ag's hsub; the gather loop un-swaps)
+    constexpr bool kHalfSwap = OT == 16 && !DUP && V == 1 && kSmemSheet && !SLAB;
     constexpr bool kLocate = MODE == kModeFused || MODE == kModeGlobal;  // in-kernel locate
     constexpr bool kPix = MODE == kModePixel;
     if constexpr (kLocate) {
@@ -586,8 +596,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 if constexpr (kPix) {
                     ag = make_float2(__int_as_float(prec[k].x), __int_as_float(prec[k].y));
                     packed = prec[k].z;
+                    if constexpr (kHalfSwap) {  // pixel records are plain: swap for this row's lane group
+                        const int n = packed / NS, sw = (n & 1) != (lane & 1);
+                        packed = (sw << kSwapBit) | ((n + sw) * NS);
+                    }
                 } else {
-                    if (xrow[k]) packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, NS, H, ag);
+                    // the lane group gathering row q has parity q & 1 = lane & 1
+                    if (xrow[k])
+                        packed = locate_ag<XT>(xa[k], xb[k], thr, pts, inv, G, gc.L, NS, H, ag, kHalfSwap ? (lane & 1) : -1);
                 }
                 const int qc = warp * Sh::ROWS_W + q;
                 rec_w[qc] = ag;
@@ -602,13 +618,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[j][v] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int rstride = (G + 1) * NS;  // node (i1+1, i2) is (G+1) nodes further
-    // conflict-free loads of plain (not duplicated) OT = 16 sheets by bank-half
-    // swapping (see the gather loop); LMKAN_B200_HALFSWAP=0 builds without
-#ifndef LMKAN_B200_HALFSWAP
-#define LMKAN_B200_HALFSWAP 1
-#endif
-    constexpr bool kHalfSwap = LMKAN_B200_HALFSWAP && OT == 16 && !DUP && V == 1 && kSmemSheet;
-    const bool gpar = ((G + 1) & 1) != 0;  // rows i1 and i1 + 1 of a node pair on opposite halves
     // The planner makes Rt a multiple of ROWS_W, so a warp's rows are all inside
     // the tile or all beyond it: warps beyond it issue no gathers. Rows past the
     // batch end inside the last tile gather zero-weight records (no branch in
@@ -754,21 +763,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
                             float4 p00, p01, p10, p11;
                             if constexpr (kHalfSwap) {
                                 // plain OT = 16 sheet: node n's 64-B run sits on bank half
-                                // (address / 64) & 1, n + 1 on the other. Each lane group
-                                // loads first the member of {n, n+1} (and of
-                                // {n+G+1, n+G+2}) on ITS half (sub & 1), so every LDS puts
-                                // 4 rows on each half (4 wavefronts, no conflicts), then
-                                // un-swaps in registers: the FMA order stays p00, p10, p01, p11.
-                                const bool sw0 = ((smem_addr(b0) >> 6) & 1u) != static_cast<uint32_t>(sub & 1);
-                                const bool sw1 = sw0 != gpar;
-                                const float4 r0 = *reinterpret_cast<const float4*>(sw0 ? b0 + NS : b0);
-                                const float4 r1 = *reinterpret_cast<const float4*>(sw1 ? b1 + NS : b1);
-                                const float4 r2 = *reinterpret_cast<const float4*>(sw0 ? b0 : b0 + NS);
-                                const float4 r3 = *reinterpret_cast<const float4*>(sw1 ? b1 : b1 + NS);
-                                p00 = sw0 ? r2 : r0;
-                                p01 = sw0 ? r0 : r2;
-                                p10 = sw1 ? r3 : r1;
-                                p11 = sw1 ? r1 : r3;
+                                // n & 1, n + 1 on the other. The record names the member
+                                // of {n, n+1} on the lane group's own half (sub & 1) and
+                                // flags sw when that is n + 1 (locate_ag); the same shift
+                                // applies to {n+G+1, n+G+2}, whose halves flip uniformly
+                                // for all lanes. So every LDS puts 4 rows on each half (4
+                                // wavefronts, no conflicts); the registers are un-swapped
+                                // so the FMA order stays p00, p10, p01, p11.
+                                const bool sw = (offs[j] >> kSwapBit) & 1;
+                                const float* f0 = sh + (offs[j] & kOffMask);
+                                const float* f1 = f0 + rstride;
+                                const int d = sw ? -NS : NS;
+                                const float4 r0 = *reinterpret_cast<const float4*>(f0);
+                                const float4 r1 = *reinterpret_cast<const float4*>(f1);
+                                const float4 r2 = *reinterpret_cast<const float4*>(f0 + d);
+                                const float4 r3 = *reinterpret_cast<const float4*>(f1 + d);
+                                p00 = sw ? r2 : r0;
+                                p01 = sw ? r0 : r2;
+                                p10 = sw ? r3 : r1;
+                                p11 = sw ? r1 : r3;
                             } else if constexpr (kSmemSheet) {
                                 p00 = *reinterpret_cast<const float4*>(b0 + vofs(v));
                                 p01 = *reinterpret_cast<const float4*>(b0 + vofs(v) + NS);

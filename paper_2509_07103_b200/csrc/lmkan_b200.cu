@@ -288,10 +288,17 @@ struct ChainLink {
 
 // K1: the cell records of `rows` rows in K2's order (records4_kernel, or the
 // shared-memory-tile records_kernel when reg4 is false).
+// Records for the bank-half-swapped gather (plain OT = 16 sheets, unslabbed,
+// shared-memory sheets: fwd_fused_kernel's kHalfSwap) carry the swap (locate_ag).
+bool half_swap(const lmkan_b200_layer* L, const Plan& pl) {
+    return L->OT == 16 && !L->dup && !L->narrow && pl.S == 1 && pl.mode != kModeGlobal;
+}
+
 template <typename XT>
 void launch_records(const lmkan_b200_layer* L, const Plan& pl, const XT* X, int64_t rows, const InputMap& im,
                     float2* recW, int* recO, bool reg4, cudaStream_t st) {
     const int H = (L->G + pl.S - 1) / pl.S;
+    const int hs = half_swap(L, pl) ? 1 : 0;
     if (reg4) {  // register-direct K1 (records4_kernel)
         const int64_t py = (L->pairs + 3) / 4;
         const int64_t gx = std::min<int64_t>((pl.rows_pad + 255) / 256,
@@ -302,20 +309,20 @@ void launch_records(const lmkan_b200_layer* L, const Plan& pl, const XT* X, int6
                          (im.conv ? (im.C % 8 == 0) : (L->n_in % 8 == 0));
         if (pl.row_tile < pl.sh.R)
             records4_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
-                                                          recO, im, pl.row_tile, vec ? 1 : 0);
+                                                          recO, im, pl.row_tile, vec ? 1 : 0, hs);
         else
             records4_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW,
-                                                           recO, im, pl.row_tile, vec ? 1 : 0);
+                                                           recO, im, pl.row_tile, vec ? 1 : 0, hs);
     } else {
         const int64_t py = (L->pairs + 15) / 16;
         const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         if (pl.row_tile < pl.sh.R)
             records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                         im, pl.row_tile);
+                                                         im, pl.row_tile, hs);
         else
             records_kernel<XT, false><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
-                                                          im, pl.row_tile);
+                                                          im, pl.row_tile, hs);
     }
 }
 
@@ -474,14 +481,15 @@ int records_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t*
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, kNumSMs * 16));
     float2* out_ag = reinterpret_cast<float2*>(ag);
     if (variant == 2) {
-        int H = L->G;
+        int H = L->G, hs = 0;
         if (!L->narrow) {
             Plan pl;
             if (!make_plan(L, rows, cap, pl, kModeFused) && !make_plan(L, rows, cap, pl, kModeGlobal))
                 return fail(LMKAN_B200_EINVAL, "records: no fused plan");
             H = (L->G + pl.S - 1) / pl.S;
+            hs = half_swap(L, pl) ? 1 : 0;
         }
-        locate_ag_kernel<XT><<<blocks, 256, 0, st>>>(X, rows, L->n_in, L->gc, L->ns, H, i1, i2, out_ag);
+        locate_ag_kernel<XT><<<blocks, 256, 0, st>>>(X, rows, L->n_in, L->gc, L->ns, H, hs, i1, i2, out_ag);
         CK(cudaGetLastError());
         return LMKAN_B200_OK;
     }
@@ -681,6 +689,7 @@ bool chain_fusable(const lmkan_b200_layer* A, const Plan& pa, const lmkan_b200_l
     if (pa.mode == kModeNarrow || A->device != B->device) return false;
     if (A->pair_block > 0) return false;  // the running sum lives in the (skipped) activation rows
     if (!make_plan(B, rows, cap, pb) || pb.mode != kModeStaged) return false;
+    if (half_swap(B, pb)) return false;  // the emitter writes plain (unswapped) records
     if (pa.row_tile != pa.sh.R || pb.row_tile != pb.sh.R) return false;  // the emitter assumes full row tiles
     const lmkan_b200_layer* ls[2] = {A, B};
     const Plan* ps[2] = {&pa, &pb};

@@ -121,13 +121,24 @@ constexpr int kOffMask = (1 << kSlabShift) - 1;
 // and a + b = h1, c + d = h2 (weights_ag). Two floats per record instead of
 // four: one 1-wavefront LDS.64 per row in the gather loop. Returns the packed
 // slab / node offset.
+//
+// hsub >= 0 (bank-half-swapped plain OT = 16 sheets, see fwd_fused_kernel):
+// the row is gathered by a lane group of parity hsub; node n's 64-B run sits on
+// bank half n & 1 (sheet slots are 128-B aligned), so the packed offset names
+// the member of {n, n+1} on the lane group's own half, n + sw, with
+// sw = (n & 1) != hsub flagged in bit kSwapBit (unslabbed sheets only).
+constexpr int kSwapBit = 30;
 template <typename XT>
 __device__ __forceinline__ int locate_ag(XT x1, XT x2, const XT* thr, const double* pts, const double* invh, int G,
-                                         int L, int OT, int H, float2& ag) {
+                                         int L, int OT, int H, float2& ag, int hsub = -1) {
     const int i1 = cell_index_fast<XT>(x1, thr, G, L);
     const int i2 = cell_index_fast<XT>(x2, thr, G, L);
     ag.x = __double2float_rn(__dmul_rn(__dsub_rn(pts[i1 + 1], static_cast<double>(x1)), invh[i1]));
     ag.y = __double2float_rn(__dmul_rn(__dsub_rn(pts[i2 + 1], static_cast<double>(x2)), invh[i2]));
+    if (hsub >= 0) {
+        const int n = i1 * (G + 1) + i2, sw = (n & 1) != hsub;
+        return (sw << kSwapBit) | ((n + sw) * OT);
+    }
     if (H >= G) return (i1 * (G + 1) + i2) * OT;  // unslabbed sheet (the common case)
     const int s = (i1 >= H) + (i1 >= 2 * H) + (i1 >= 3 * H);  // slab (S <= 4), no integer division
     return (s << kSlabShift) | (((i1 - s * H) * (G + 1) + i2) * OT);
