@@ -156,15 +156,25 @@ int lmkan_b200_forward_f32_dests(const lmkan_b200_layer* layer, const float* X_d
 int lmkan_b200_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
 int lmkan_b200_ipc_open_handle(const void* handle, uint64_t offset, int device, void** dev_ptr);
 int lmkan_b200_ipc_close(void* dev_ptr);
-/* Device-side barrier after the fused gather, on the same stream: rank
- * `rank` of `world` (<= 8) stores `epoch` (> 0, increasing) into slot `rank`
- * of every rank's int32[world] flag array (flag_arrays[q], IPC-mapped;
- * system-scope release after a system fence) and spins until all slots of its
- * own array reach `epoch` (acquire). status_dev (int32, device) is set to
- * 1 + q if peer q did not arrive within timeout_ms (<= 0: 10 s), else left
- * unchanged. */
+/* Device-side barrier on a stream: rank `rank` of `world` (<= 8) stores
+ * `epoch` (> 0, increasing) into slot `rank` of every rank's int32[world] flag
+ * array (flag_arrays[q], IPC-mapped; system-scope release after a system
+ * fence) and spins until all slots of its own array reach `epoch` (acquire).
+ * status (int32, device memory or pinned host memory) is set to 1 + q if peer
+ * q did not arrive within timeout_ms (<= 0: 10 s), else left unchanged.
+ * PeerGather (sharding.py) enqueues one before the fused forward (no rank
+ * stores into a peer's Y before that peer's earlier stream work has consumed
+ * it) and one after it (every rank's columns have landed). */
 int lmkan_b200_peer_barrier(int* const* flag_arrays, int world, int rank, int epoch, int timeout_ms,
                             int* status_dev, void* stream);
+
+/* Explicit peer access for the fused all-gather (instead of relying on the
+ * lazy enable of cudaIpcOpenMemHandle): the PCI bus id of `device`
+ * ("0000:1b:00.0", buf >= 13 bytes), and a check + enable of access from
+ * `device` to the GPU with that bus id. EUNSUPPORTED with an explicit message
+ * when the pair has no peer path (or the peer is not visible here). */
+int lmkan_b200_device_pci_bus_id(int device, char* buf, int len);
+int lmkan_b200_peer_access(int device, const char* peer_pci_bus_id);
 
 /* Drop-in synchronous host paths: X/Y in host memory (pinned or pageable),
  * copies and kernels pipelined over row chunks on internal streams; returns

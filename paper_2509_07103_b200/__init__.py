@@ -364,10 +364,25 @@ def ipc_close(ptr: int) -> None:
 
 
 def peer_barrier(flag_ptrs, rank: int, epoch: int, status, timeout_ms: int = 10000, stream=None) -> None:
-    """Enqueue the device-side barrier (see include/lmkan_b200.h)."""
+    """Enqueue the device-side barrier (see include/lmkan_b200.h); `status` is
+    an int32 tensor on the device or in pinned host memory."""
     arr = (C.c_void_p * len(flag_ptrs))(*[int(p) for p in flag_ptrs])
     check(lib.lmkan_b200_peer_barrier(arr, len(flag_ptrs), int(rank), int(epoch), int(timeout_ms),
                                       C.c_void_p(status.data_ptr()), _stream_ptr(stream)))
+
+
+def device_pci_bus_id(device: int) -> str:
+    buf = C.create_string_buffer(32)
+    check(lib.lmkan_b200_device_pci_bus_id(int(device), buf, 32))
+    return buf.value.decode()
+
+
+def peer_access(device: int, peer_pci_bus_id: str) -> None:
+    """Check and enable peer access from `device` to the GPU with that PCI bus
+    id; RuntimeError naming both GPUs if the pair has no peer path."""
+    rc = lib.lmkan_b200_peer_access(int(device), peer_pci_bus_id.encode())
+    if rc != 0:
+        raise RuntimeError((lib.lmkan_b200_last_error() or b"").decode())
 
 
 # ---------------------------------------------------------------------------

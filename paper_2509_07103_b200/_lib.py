@@ -48,6 +48,8 @@ _SIGS = [
      [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("lmkan_b200_conv_forward_host_f32", C.c_int,
      [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
+    ("lmkan_b200_device_pci_bus_id", C.c_int, [C.c_int, C.c_char_p, C.c_int]),
+    ("lmkan_b200_peer_access", C.c_int, [C.c_int, C.c_char_p]),
     ("lmkan_b200_forward_host_f64", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
     ("lmkan_b200_forward_host_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_size_t]),
     ("lmkan_b200_locate_f32", C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P]),

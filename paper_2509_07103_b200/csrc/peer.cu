@@ -8,6 +8,7 @@
 // until every slot of its own array holds `epoch` (acquire). A bounded spin
 // turns a missing peer into an error instead of a hung GPU.
 #include <cstdint>
+#include <string>
 
 #include "../../include/lmkan_b200.h"
 #include "layer_impl.hpp"
@@ -69,6 +70,43 @@ int lmkan_b200_peer_barrier(int* const* flag_arrays, int world, int rank, int ep
     peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(fp, world, rank, epoch, cycles, status_dev);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return api::cuda_error(e, "peer_barrier: launch");
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_device_pci_bus_id(int device, char* buf, int len) {
+    if (!buf || len < 13) return api::set_error(LMKAN_B200_EINVAL, "device_pci_bus_id: buffer too small");
+    const cudaError_t e = cudaDeviceGetPCIBusId(buf, len, device);
+    if (e != cudaSuccess) return api::cuda_error(e, "device_pci_bus_id");
+    return LMKAN_B200_OK;
+}
+
+int lmkan_b200_peer_access(int device, const char* peer_pci_bus_id) {
+    if (!peer_pci_bus_id) return api::set_error(LMKAN_B200_EINVAL, "peer_access: null PCI bus id");
+    int peer = -1;
+    if (cudaDeviceGetByPCIBusId(&peer, peer_pci_bus_id) != cudaSuccess || peer < 0) {
+        cudaGetLastError();
+        return api::set_error(LMKAN_B200_EUNSUPPORTED, std::string("peer_access: GPU ") + peer_pci_bus_id +
+                                                           " is not visible to this process (CUDA_VISIBLE_DEVICES)");
+    }
+    if (peer == device) return LMKAN_B200_OK;
+    int can = 0;
+    cudaError_t e = cudaDeviceCanAccessPeer(&can, device, peer);
+    if (e != cudaSuccess) return api::cuda_error(e, "peer_access: cudaDeviceCanAccessPeer");
+    if (!can)
+        return api::set_error(LMKAN_B200_EUNSUPPORTED, "peer_access: GPU " + std::to_string(device) +
+                                                           " cannot access GPU " + std::to_string(peer) +
+                                                           " (no NVLink / PCIe peer path): the fused all-gather "
+                                                           "needs peer access, use the NCCL gather instead");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    e = cudaDeviceEnablePeerAccess(peer, 0);
+    cudaSetDevice(prev);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        e = cudaSuccess;
+    }
+    if (e != cudaSuccess) return api::cuda_error(e, "peer_access: cudaDeviceEnablePeerAccess");
     return LMKAN_B200_OK;
 }
 

@@ -18,6 +18,7 @@ summation order does not depend on the partition).
 """
 from __future__ import annotations
 
+import os
 from typing import Callable, List, Optional, Tuple
 
 
@@ -92,16 +93,29 @@ class PeerGather:
     """Full-width output buffer shared by all ranks of an output-sharded layer.
 
     Every rank allocates Y [rows, n_out] and an int32 flag array, publishes
-    CUDA IPC handles (all_gather_object), and maps the peers' buffers. Then
-    ``forward(layer, X, col0)`` runs the rank's shard with the library's
-    multi-destination epilogue (lmkan_b200_forward_f32_dests: the tile of
-    every CTA is stored into all ranks' Y over NVLink as it completes) followed
-    by lmkan_b200_peer_barrier on the same stream, after which Y holds every
-    rank's columns on every GPU — the all-gather fused into the compute, no
-    separate collective. Device pointers only; ranks must be GPUs of one node.
+    CUDA IPC handles (all_gather_object), checks and enables peer access to
+    every peer GPU explicitly (an error naming the pair if there is no peer
+    path), and maps the peers' buffers. ``forward(layer, X, col0)`` then
+    enqueues on the stream:
+
+      1. an ENTRY barrier (lmkan_b200_peer_barrier, epoch 2e - 1): no rank
+         stores into a peer's Y before that peer has arrived here, i.e. before
+         the peer's earlier work on its stream — the consumers of the previous
+         result — has completed (no cross-GPU write-after-read);
+      2. the rank's shard with the multi-destination epilogue
+         (lmkan_b200_forward_f32_dests, this rank's own Y first: each CTA's tile
+         is stored into every rank's Y over NVLink as it completes);
+      3. an EXIT barrier (epoch 2e): every rank's columns have landed.
+
+    After step 3 Y holds the whole output on every GPU — the all-gather fused
+    into the compute, no separate collective. Y is valid for consumers on the
+    same stream (or ordered after it) until the next forward. A rank that does
+    not arrive within the timeout sets the pinned host status word, and the
+    next forward() / check() raises. Device pointers only; ranks must be GPUs
+    of one node.
     """
 
-    def __init__(self, rows: int, n_out: int, device: int, group=None):
+    def __init__(self, rows: int, n_out: int, device: int, group=None, timeout_ms: int = 10000):
         import torch
         import torch.distributed as dist
         import paper_2509_07103_b200 as pkg
@@ -112,41 +126,56 @@ class PeerGather:
             raise ValueError("PeerGather: at most 8 ranks (one NVLink domain)")
         self.device = device
         self.n_out = n_out
+        self.timeout_ms = timeout_ms
         self.Y = torch.empty((rows, n_out), dtype=torch.float32, device=f"cuda:{device}")
         self.flags = torch.zeros(self.world, dtype=torch.int32, device=f"cuda:{device}")
-        self.status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
-        mine = (pkg.ipc_handle(self.Y), pkg.ipc_handle(self.flags))
+        # barrier timeouts land in pinned host memory: readable without a sync
+        self.status = torch.zeros(1, dtype=torch.int32).pin_memory()
+        mine = (pkg.ipc_handle(self.Y), pkg.ipc_handle(self.flags), pkg.device_pci_bus_id(device))
         everyone = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(everyone, mine, group=group)
         else:
             everyone = [mine]
+        for q, (_, _, bus) in enumerate(everyone):
+            if q != self.rank:
+                pkg.peer_access(device, bus)  # explicit: fails loudly without a peer path
         self._opened: List[int] = []
-        self.y_ptrs, self.flag_ptrs = [], []
-        for q, ((hy, oy), (hf, of)) in enumerate(everyone):
+        peer_y, self.flag_ptrs = {}, []
+        for q, ((hy, oy), (hf, of), _) in enumerate(everyone):
             if q == self.rank:
-                self.y_ptrs.append(self.Y.data_ptr())
                 self.flag_ptrs.append(self.flags.data_ptr())
             else:
                 py, pf = pkg.ipc_open(hy, oy, device), pkg.ipc_open(hf, of, device)
                 self._opened += [py, pf]
-                self.y_ptrs.append(py)
+                peer_y[q] = py
                 self.flag_ptrs.append(pf)
+        # this rank's own Y first (the kernel keeps pair-block running sums in dests[0])
+        self.y_ptrs = [self.Y.data_ptr()] + [peer_y[q] for q in sorted(peer_y)]
         self.epoch = 0
+        # LMKAN_B200_PEER_ENTRY_BARRIER=0 drops the entry barrier (only to show
+        # the back-to-back test catches the write-after-read race without it)
+        self._entry = os.environ.get("LMKAN_B200_PEER_ENTRY_BARRIER", "1") != "0"
         if self.world > 1:
             dist.barrier(group=group)  # every mapping exists before anyone stores into it
 
     def forward(self, layer, X, col0: int, stream=None):
         """This rank's columns [col0, col0 + layer.n_out) into every rank's Y,
-        then the device-side barrier; returns the (full) local Y."""
-        layer.forward_dests(X, self.y_ptrs, self.n_out, col0, stream)
+        between an entry and an exit barrier; returns the (full) local Y."""
+        self.check()
         self.epoch += 1
-        self._pkg.peer_barrier(self.flag_ptrs, self.rank, self.epoch, self.status, stream=stream)
+        if self._entry:
+            self._pkg.peer_barrier(self.flag_ptrs, self.rank, 2 * self.epoch - 1, self.status, self.timeout_ms,
+                                   stream=stream)
+        layer.forward_dests(X, self.y_ptrs, self.n_out, col0, stream)
+        self._pkg.peer_barrier(self.flag_ptrs, self.rank, 2 * self.epoch, self.status, self.timeout_ms,
+                               stream=stream)
         return self.Y
 
     def check(self) -> None:
-        """Raise if a barrier timed out (call after synchronizing the stream)."""
-        st = int(self.status.item())
+        """Raise if a barrier of an earlier forward timed out (no sync needed:
+        the status word is pinned host memory written by the barrier kernel)."""
+        st = int(self.status[0])
         if st:
             raise RuntimeError(f"PeerGather: rank {st - 1} did not arrive at the barrier")
 

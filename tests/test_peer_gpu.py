@@ -133,3 +133,67 @@ def test_peer_gather_two_processes(torch):
             p.kill()
     assert codes == [0, 0], codes
     assert q.get(timeout=5) is True
+
+
+def _rank_back_to_back(rank, world, port, n_in, n_out, G, rows, steps, out_q):
+    """Steps back to back with no host barrier; rank 0 consumes each result
+    slowly (a 20 ms sleep before copying Y) while rank 1 runs ahead: the entry
+    barrier must keep rank 1 from storing step e+1 into rank 0's Y before rank
+    0 has read step e."""
+    import torch
+    import torch.distributed as dist
+    import paper_2509_07103_b200 as pkg
+    from paper_2509_07103_b200 import sharding
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ob, oe = sharding.shard_range(n_out, rank, world, align=16)
+    lay = pkg.Layer.random(n_in, n_out, G, seed=12, out_range=(ob, oe))
+    Xs = [torch.randn((rows, n_in), generator=torch.Generator().manual_seed(100 + e)).cuda() for e in range(steps)]
+    pg = sharding.PeerGather(rows, n_out, 0)
+    st = torch.cuda.Stream()
+    hist = []
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        for e in range(steps):
+            Y = pg.forward(lay, Xs[e], ob, st)
+            if rank == 0:
+                torch.cuda._sleep(40_000_000)  # a slow consumer of step e's result
+            hist.append(Y.clone())
+    st.synchronize()
+    pg.check()
+    if rank == 0:
+        full = pkg.Layer.random(n_in, n_out, G, seed=12)
+        out_q.put(all(bool(torch.equal(h, full.forward(x))) for h, x in zip(hist, Xs)))
+    dist.barrier()
+    pg.close()
+    dist.destroy_process_group()
+
+
+def test_peer_gather_back_to_back_steps(torch):
+    """No cross-GPU write-after-read on Y across consecutive forwards (entry
+    barrier), with no host synchronisation between the steps."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = (2, port, 64, 64, 8, 3000, 6, q)
+    procs = [ctx.Process(target=_rank_back_to_back, args=(r,) + args) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    codes = [p.exitcode for p in procs]
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    assert codes == [0, 0], codes
+    assert q.get(timeout=5) is True
+
+
+def test_peer_access_checks(torch, pkg):
+    own = pkg.device_pci_bus_id(0)
+    assert len(own) >= 12
+    pkg.peer_access(0, own)  # a device and itself: nothing to enable
+    with pytest.raises(RuntimeError, match="not visible"):
+        pkg.peer_access(0, "0000:ff:1f.7")
