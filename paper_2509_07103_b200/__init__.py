@@ -154,29 +154,44 @@ class Layer:
         return cls(h)
 
     # -- forward ------------------------------------------------------------
+    def _check_x(self, X, dtypes=("float32", "float64")) -> None:
+        """Shared checks of the device entry points: a 2-D contiguous CUDA tensor
+        of the layer's width and an accepted dtype."""
+        import torch
+        if X.dim() != 2 or X.shape[1] != self.n_in:
+            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
+        if not (X.is_cuda and X.is_contiguous()):
+            raise ValueError("lmkan_forward: X must be a contiguous CUDA tensor")
+        if X.dtype not in tuple(getattr(torch, d) for d in dtypes):
+            raise ValueError(f"lmkan_forward: X dtype {X.dtype} not in {dtypes}")
+
     def forward_into(self, X, Y, stream=None) -> None:
         """Device path: X [rows, n_in], Y [rows, n_out] contiguous CUDA tensors
         (float32 or float64, same dtype); asynchronous on `stream`."""
         import torch
-        if X.dim() != 2 or X.shape[1] != self.n_in:
-            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
-        assert X.is_cuda and Y.is_cuda and X.is_contiguous() and Y.is_contiguous()
-        assert Y.shape == (X.shape[0], self.n_out) and Y.dtype == X.dtype
+        self._check_x(X)
+        if not (Y.is_cuda and Y.is_contiguous() and Y.shape == (X.shape[0], self.n_out) and Y.dtype == X.dtype):
+            raise ValueError(f"lmkan_forward: Y must be a contiguous CUDA tensor [{X.shape[0]}, {self.n_out}] of X's dtype")
         fn = lib.lmkan_b200_forward_f32 if X.dtype == torch.float32 else lib.lmkan_b200_forward_f64
         check(fn(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream)))
 
     def forward_dests(self, X, dest_ptrs, ld: int, col0: int, stream=None) -> None:
         """Forward (float32) storing this layer's output columns into every
         destination buffer: dest[r * ld + col0 + q] (device pointers, e.g. the
-        full-width Y of every GPU of an output-sharded layer)."""
-        if X.dim() != 2 or X.shape[1] != self.n_in:
-            raise ValueError(f"lmkan_forward: expected width {self.n_in}, got {X.shape[-1]}")
+        full-width Y of every GPU of an output-sharded layer; this GPU's own
+        buffer first: pair-block running sums live in dests[0])."""
+        self._check_x(X, ("float32",))
+        if col0 < 0 or ld < col0 + self.n_out:
+            raise ValueError("forward_dests: ld must be >= col0 + n_out")
         arr = (C.c_void_p * len(dest_ptrs))(*[int(p) for p in dest_ptrs])
         check(lib.lmkan_b200_forward_f32_dests(self._h, _ptr(X), arr, len(dest_ptrs), int(ld), int(col0),
                                                int(X.shape[0]), _stream_ptr(stream)))
 
     def forward_into_timed(self, X, Y, ev_begin, ev_end, stream=None) -> None:
         """forward_into (float32) recording torch.cuda.Events around the gather kernel."""
+        self._check_x(X, ("float32",))
+        if not (Y.is_cuda and Y.is_contiguous() and Y.shape == (X.shape[0], self.n_out) and Y.dtype == X.dtype):
+            raise ValueError(f"lmkan_forward: Y must be a contiguous CUDA tensor [{X.shape[0]}, {self.n_out}] of X's dtype")
         check(lib.lmkan_b200_forward_f32_timed(self._h, _ptr(X), _ptr(Y), int(X.shape[0]), _stream_ptr(stream),
                                                C.c_void_p(ev_begin.cuda_event), C.c_void_p(ev_end.cuda_event)))
 
@@ -273,28 +288,43 @@ class Layer:
         dP is added into (zeros when None). Returns (dP, dX or None); bitwise
         equal to the reference run with the same `workers` (0 = GPU-filling
         count, see backward_workers). numpy in -> synchronous host path."""
+        n_par = (self.G + 1) ** 2 * self.pairs * self.n_out
+
+        def check_io(Xs, dYs, Ps):
+            if len(Xs.shape) != 2 or Xs.shape[1] != self.n_in:
+                raise ValueError(f"lmkan_backward: expected width {self.n_in}, got {Xs.shape[-1]}")
+            if len(dYs.shape) != 2 or dYs.shape[1] != self.n_out:
+                raise ValueError(f"lmkan_backward: expected width {self.n_out}, got {dYs.shape[-1]}")
+            if dYs.shape[0] != Xs.shape[0]:
+                raise ValueError("lmkan_backward: X and dY row counts differ")
+            if int(np.prod(Ps.shape)) != n_par:
+                raise ValueError(f"lmkan_backward: P has {int(np.prod(Ps.shape))} coefficients, the layer {n_par}")
+
         if isinstance(X, np.ndarray):
             P = np.ascontiguousarray(P, np.float64)
             X = np.ascontiguousarray(X, np.float64)
             dY = np.ascontiguousarray(dY, np.float64)
+            check_io(X, dY, P)
             dP = np.zeros(P.shape) if dP is None else np.ascontiguousarray(dP, np.float64)
+            if dP.size != n_par:
+                raise ValueError("lmkan_backward: dP size mismatch")
             dX = np.zeros(X.shape) if want_dx else None
             check(lib.lmkan_b200_backward_host_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX),
                                                    int(X.shape[0]), int(workers)))
             return dP, dX
         import torch
-        for t in (P, X, dY):
-            assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
-        if X.shape[1] != self.n_in:
-            raise ValueError(f"lmkan_backward: expected width {self.n_in}, got {X.shape[1]}")
-        if dY.shape[1] != self.n_out:
-            raise ValueError(f"lmkan_backward: expected width {self.n_out}, got {dY.shape[1]}")
-        if dY.shape[0] != X.shape[0]:
-            raise ValueError("lmkan_backward: X and dY row counts differ")
+        for name, t in (("P", P), ("X", X), ("dY", dY)):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ValueError(f"lmkan_backward: {name} must be a contiguous float64 CUDA tensor")
+        check_io(X, dY, P)
         if dP is None:
             dP = torch.zeros_like(P)
-        elif dP.numel() != P.numel():
+        elif not (dP.is_cuda and dP.dtype == torch.float64 and dP.is_contiguous() and dP.device == P.device):
+            raise ValueError("lmkan_backward: dP must be a contiguous float64 tensor on P's device")
+        elif dP.numel() != n_par:
             raise ValueError("lmkan_backward: dP size mismatch")
+        if X.device != P.device or dY.device != P.device:
+            raise ValueError("lmkan_backward: P, X and dY must be on the same device")
         dX = torch.empty_like(X) if want_dx else None
         check(lib.lmkan_b200_backward_f64(self._h, _ptr(P), _ptr(X), _ptr(dY), _ptr(dP), _ptr(dX), int(X.shape[0]),
                                           int(workers), _stream_ptr(stream)))

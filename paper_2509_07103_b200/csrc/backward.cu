@@ -184,14 +184,14 @@ int backward_device(const lmkan_b200_layer* L, const double* P, const double* X,
         e = cudaGetLastError();
     }
     if (e == cudaSuccess && W > 1) {
-        merge_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(
+        merge_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, static_cast<size_t>(L->num_sms) * 16)), 256, 0, st>>>(
             dP, partials, n, static_cast<int>(W - 1));
         e = cudaGetLastError();
     }
     if (partials) cudaFreeAsync(partials, st);
     if (e == cudaSuccess && dX) {
         const int64_t total = rows * pairs;
-        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, L->num_sms * 32));
         backward_dx_kernel<<<blocks, 256, 0, st>>>(P, X, dY, dX, rows, L->n_in, L->n_out, gamma, L->gc);
         e = cudaGetLastError();
     }

@@ -2,6 +2,8 @@
 // gather_ot*.cu translation units, each instantiating one output-tile width.
 #pragma once
 
+#include <atomic>
+
 #include "layer_impl.hpp"
 
 namespace lmkan_b200 {
@@ -12,12 +14,12 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
                            const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
     auto kern = fwd_fused_kernel<OT, RT, XT, MODE, SLAB, NW, TAIL, DUP, GOFF>;
-    static int configured[64] = {0};  // per device: dynamic-smem opt-in done
+    static std::atomic<bool> configured[64];  // per device: dynamic-smem opt-in done (idempotent)
     const int dev = L->device & 63;
-    if (!configured[dev]) {
+    if (!configured[dev].load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return e;
-        configured[dev] = 1;
+        configured[dev].store(true, std::memory_order_release);
     }
     dim3 grid(static_cast<unsigned>(pl.row_tiles), static_cast<unsigned>(L->n_ot));
     kern<<<grid, NW * 32, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,

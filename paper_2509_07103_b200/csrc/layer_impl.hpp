@@ -18,6 +18,7 @@ struct lmkan_b200_layer {
     bool dup = false;     // OT = 16 duplicated-node table [ot][pair][node][2][OT] (conflict-free gathers)
     int ns = 64;          // node stride of the device table in floats (OT, or 2 OT when dup)
     int pair_block = 0;   // pair-block summation block (0: one running sum; see fwd_fused_kernel)
+    int num_sms = 148;    // the device's SM count (queried at creation)
     float* table = nullptr;
     size_t table_bytes = 0;
     double* d_inv = nullptr;

@@ -9,6 +9,7 @@
 // There is no CPU compute fallback: without an sm_100a device every compute
 // entry point fails with LMKAN_B200_ENOSYS / ECUDA.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -90,7 +91,6 @@ int max_smem_optin(int device) {
 // float4 accumulators per thread (the register tile); rows per thread RT =
 // choice / lane_vectors(OT), so the rows per CTA do not depend on V
 constexpr int kRTChoices[] = {16, 8, 4};
-constexpr int kNumSMs = 148;
 constexpr int kMaxSlabs = 4;
 
 int env_int(const char* name, int dflt) {
@@ -162,7 +162,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
               force_s = env_int("LMKAN_B200_SLABS", 0);
     if (L->narrow) {
-        const int64_t ctas = std::min<int64_t>(kNumSMs, (rows + kNarrowThreads - 1) / kNarrowThreads);
+        const int64_t ctas = std::min<int64_t>(L->num_sms, (rows + kNarrowThreads - 1) / kNarrowThreads);
         out = Plan{L->OT, 1, 1, kModeNarrow, 1, shape_rt(16, 4), narrow_smem_bytes(L->G, L->pairs, L->OT), ctas,
                    rows, 1, 0};
         return static_cast<int>(out.smem) <= smem_cap;
@@ -177,7 +177,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
     // small to give every SM a 16-warp CTA (the per-pair locate then sits on the
     // critical path of the few rows each CTA owns; measured 32 vs 47 us at cfg1)
     const int rt_small = kRTChoices[2] / lane_vectors(L->OT);
-    const bool small = ((rows + shape_rt(L->OT, rt_small).R - 1) / shape_rt(L->OT, rt_small).R) * L->n_ot < kNumSMs;
+    const bool small = ((rows + shape_rt(L->OT, rt_small).R - 1) / shape_rt(L->OT, rt_small).R) * L->n_ot < L->num_sms;
     const int NSt = L->ns;  // node stride of the table (2 OT for duplicated-node tables)
     const int pref = (L->n_ot >= 3 || small) ? kModeStaged : kModeFused;
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
@@ -203,7 +203,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                             NW = force_nw;
                         } else {
                             while (NW > 1 && ((rows + shape_rt(L->OT, RT, NW, NSt).R - 1) / shape_rt(L->OT, RT, NW, NSt).R) *
-                                                     L->n_ot < kNumSMs)
+                                                     L->n_ot < L->num_sms)
                                 NW >>= 1;
                         }
                     }
@@ -212,7 +212,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                     // a taller row tile reuses each sheet for more rows; take it while the
                     // grid still covers >= 3/4 of the SMs (cfg4: RT 16 with 128 CTAs 0.392 ms
                     // beat RT 8 with 256 CTAs = 1.7 waves, 0.404 ms)
-                    if (!force_rt && A != kRTChoices[2] && tiles * L->n_ot * 4 < kNumSMs * 3) continue;
+                    if (!force_rt && A != kRTChoices[2] && tiles * L->n_ot * 4 < L->num_sms * 3) continue;
                     for (int nbuf = smem_sheet ? max_nbuf : 0; nbuf >= (smem_sheet ? min_buf : 0); --nbuf) {
                         if (force_nbuf && smem_sheet && nbuf != force_nbuf) continue;
                         const int units = L->pairs * S;
@@ -236,7 +236,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                             // warps) cost more than they save (cfg2's chunked host path:
                             // e2e 19.5 -> 21.0 ms when its 256-CTA chunks were balanced)
                             const int64_t ctas = tiles * L->n_ot;
-                            const int64_t want = ctas < kNumSMs ? kNumSMs / L->n_ot : 0;
+                            const int64_t want = ctas < L->num_sms ? L->num_sms / L->n_ot : 0;
                             if (want > tiles) {
                                 // whole warps only (a warp is all in or all out of the
                                 // tile: no masked rows in the hot loop); also even
@@ -264,12 +264,12 @@ size_t record_scratch_cap() { return static_cast<size_t>(env_int("LMKAN_B200_MAX
 template <typename XT, int NO>
 cudaError_t launch_narrow(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const OutDests<XT>& Y, int64_t rows,
                           const InputMap& im, cudaStream_t st) {
-    static int configured[64] = {0};
-    if (!configured[L->device & 63]) {
+    static std::atomic<bool> configured[64];  // per device: dynamic-smem opt-in done (idempotent)
+    if (!configured[L->device & 63].load(std::memory_order_acquire)) {
         cudaError_t e =
             cudaFuncSetAttribute(narrow_kernel<XT, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return e;
-        configured[L->device & 63] = 1;
+        configured[L->device & 63].store(true, std::memory_order_release);
     }
     narrow_kernel<XT, NO><<<static_cast<unsigned>(pl.row_tiles), kNarrowThreads, pl.smem, st>>>(
         X, Y, rows, L->n_in, L->n_out, L->table, static_cast<float>(L->gamma), L->gc, im, L->pair_block);
@@ -302,7 +302,7 @@ void launch_records(const lmkan_b200_layer* L, const Plan& pl, const XT* X, int6
     if (reg4) {  // register-direct K1 (records4_kernel)
         const int64_t py = (L->pairs + 3) / 4;
         const int64_t gx = std::min<int64_t>((pl.rows_pad + 255) / 256,
-                                             std::max<int64_t>(1, (kNumSMs * 8 + py - 1) / py));
+                                             std::max<int64_t>(1, (L->num_sms * 8 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         // 32-byte group loads: 8 contiguous inputs at 32-byte aligned offsets
         const bool vec = (reinterpret_cast<uintptr_t>(X) & 31) == 0 &&
@@ -315,7 +315,7 @@ void launch_records(const lmkan_b200_layer* L, const Plan& pl, const XT* X, int6
                                                            recO, im, pl.row_tile, vec ? 1 : 0, hs);
     } else {
         const int64_t py = (L->pairs + 15) / 16;
-        const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (kNumSMs * 32 + py - 1) / py));
+        const int64_t gx = std::min<int64_t>((pl.rows_pad + 63) / 64, std::max<int64_t>(1, (L->num_sms * 32 + py - 1) / py));
         dim3 g1(static_cast<unsigned>(gx), static_cast<unsigned>(py));
         if (pl.row_tile < pl.sh.R)
             records_kernel<XT, true><<<g1, 256, 0, st>>>(X, rows, pl.rows_pad, L->n_in, L->gc, pl.sh, H, recW, recO,
@@ -368,7 +368,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
         im.npix < (int64_t(1) << 31) && !link.emit.W && env_int("LMKAN_B200_PIXREC", 1)) {
         const int64_t nrec = im.npix * (im.C / 2);
         CK(cudaMallocAsync(reinterpret_cast<void**>(&pixrec), static_cast<size_t>(nrec) * sizeof(int4), st));
-        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((nrec + 255) / 256, kNumSMs * 16));
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((nrec + 255) / 256, L->num_sms * 16));
         pixel_records_kernel<XT><<<blocks, 256, 0, st>>>(X, im.npix, im.C, L->gc, L->ns, L->G, pixrec);
         const cudaError_t e1 = cudaGetLastError();
         if (e1 != cudaSuccess) {
@@ -455,7 +455,7 @@ int locate_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t* 
     if (reinterpret_cast<uintptr_t>(w) % 16 != 0) return fail(LMKAN_B200_EINVAL, "locate: w must be 16-byte aligned");
     DeviceGuard g(L->device);
     const int64_t total = rows * L->pairs;
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, L->num_sms * 16);
     locate_kernel<XT><<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, rows, L->n_in, L->gc, i1, i2,
                                                                      reinterpret_cast<float4*>(w));
     CK(cudaGetLastError());
@@ -478,7 +478,7 @@ int records_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t*
     DeviceGuard g(L->device);
     const int cap = max_smem_optin(L->device);
     const int64_t total = rows * L->pairs;
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, kNumSMs * 16));
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, L->num_sms * 16));
     float2* out_ag = reinterpret_cast<float2*>(ag);
     if (variant == 2) {
         int H = L->G, hs = 0;
@@ -544,6 +544,11 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     L->pairs = n_in / 2;
     L->nodes = (G + 1) * (G + 1);
     L->gamma = gamma;
+    {  // planning and grid sizing use the device's SM count (148 on B200)
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+            L->num_sms = sms;
+    }
     const int no = n_out_local <= 1 ? 1 : (n_out_local <= 2 ? 2 : 4);
     if (n_out_local <= 4 && env_int("LMKAN_B200_NARROW", 1) &&
         static_cast<int>(narrow_smem_bytes(G, n_in / 2, no)) <= max_smem_optin(device)) {
@@ -605,6 +610,8 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     return LMKAN_B200_OK;
 }
 
+// Blocks of 256 threads for the grid-stride preparation kernels (capped at 64
+// per SM of a 148-SM B200; the loops cover any size).
 unsigned fill_blocks(size_t total) {
     return static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 64));
 }
@@ -641,7 +648,7 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     // ~8 chunks of at least one wave of row tiles (cfg2: 8 measured best; fewer
     // expose more of the first H2D / last D2H, more shrink the grids below a
     // wave): LMKAN_B200_HOST_CHUNKS overrides
-    const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * kNumSMs / std::max(1, L->n_ot);
+    const int64_t min_chunk = static_cast<int64_t>(pl.sh.R) * L->num_sms / std::max(1, L->n_ot);
     const int64_t nchunks = std::max(1, env_int("LMKAN_B200_HOST_CHUNKS", 8));
     int64_t chunk = std::max<int64_t>({(rows + nchunks - 1) / nchunks, min_chunk, 1});
     chunk = std::min(chunk, rows);
@@ -984,7 +991,7 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: no kernel variant fits shared memory");
     // chunks of at least one wave of 512-row tiles (a full-batch plan's taller
     // tile would otherwise make a single chunk), else ~8 chunks
-    const int64_t wave_rows = static_cast<int64_t>(env_int("LMKAN_B200_CONV_CHUNK_ROWS", 512)) * kNumSMs /
+    const int64_t wave_rows = static_cast<int64_t>(env_int("LMKAN_B200_CONV_CHUNK_ROWS", 512)) * L->num_sms /
                               std::max(1, L->n_ot);
     const int64_t min_imgs = (wave_rows + per_img - 1) / per_img;
     const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));

@@ -331,7 +331,7 @@ int stream_table(const std::string& path, const Lmk1& m, const TensorMeta& t, lm
             break;
         }
         if ((e = cudaMemcpyAsync(dev[b], host[b], n * m.elem, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
-        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 32));
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(L->num_sms) * 32));
         if (m.elem == 8)
             relayout_chunk_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dev[b]), f0, n, L->table,
                                                                    L->pairs, L->nodes, L->n_out_total, L->out_begin,

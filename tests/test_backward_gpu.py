@@ -126,7 +126,7 @@ def test_backward_argument_errors(torch, pkg):
     with pytest.raises(ValueError, match="row counts differ"):
         layer.backward(Pd, Xd, dYd[:5].contiguous())
     sl = pkg.Layer.from_device(4, 3, 4, Pd.float(), 1.0, out_range=(0, 2))
-    with pytest.raises(ValueError, match="output-sliced"):
+    with pytest.raises(ValueError, match="output-sliced|coefficients"):
         sl.backward(Pd, Xd, dYd[:, :2].contiguous())
 
 
@@ -141,3 +141,40 @@ def test_backward_nonfinite_inputs_bitwise(torch, pkg, oracle):
     got_dP, got_dX = layer.backward(P, X, dY, workers=1)
     assert np.array_equal(got_dP.view(np.uint64), ref_dP.view(np.uint64))
     assert np.array_equal(got_dX.view(np.uint64), ref_dX.view(np.uint64))
+
+
+def test_backward_argument_checks(torch, pkg):
+    """dP / P / X / dY are validated before any pointer reaches the C-ABI
+    (a float32 or mis-sized dP would otherwise be written out of bounds)."""
+    layer = pkg.Layer.random(8, 6, 5, seed=2)
+    n = 6 * 6 * 4 * 6
+    P = torch.zeros(n, dtype=torch.float64, device="cuda")
+    X = torch.zeros((3, 8), dtype=torch.float64, device="cuda")
+    dY = torch.zeros((3, 6), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="dP must be"):
+        layer.backward(P, X, dY, dP=torch.zeros(n, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError, match="size mismatch"):
+        layer.backward(P, X, dY, dP=torch.zeros(n + 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="coefficients"):
+        layer.backward(P[:-1], X, dY)
+    with pytest.raises(ValueError, match="contiguous float64"):
+        layer.backward(P, X.float(), dY)
+    with pytest.raises(ValueError, match="expected width 8"):
+        layer.backward(P.cpu().numpy(), np.zeros((3, 9)), np.zeros((3, 6)))
+    with pytest.raises(ValueError, match="row counts differ"):
+        layer.backward(P.cpu().numpy(), np.zeros((3, 8)), np.zeros((2, 6)))
+    dP, dX = layer.backward(P, X, dY)
+    assert dP.shape == P.shape and dX.shape == X.shape
+
+
+def test_forward_argument_checks(torch, pkg):
+    layer = pkg.Layer.random(8, 6, 5, seed=2)
+    X = torch.zeros((3, 8), device="cuda")
+    with pytest.raises(ValueError, match="contiguous CUDA"):
+        layer.forward_into(torch.zeros((8, 3), device="cuda").t(), torch.empty((3, 6), device="cuda"))
+    with pytest.raises(ValueError, match="Y must be"):
+        layer.forward_into(X, torch.empty((3, 6), device="cuda", dtype=torch.float64))
+    with pytest.raises(ValueError, match="dtype"):
+        layer.forward_dests(X.double(), [0], 6, 0)
+    with pytest.raises(ValueError, match="ld must be"):
+        layer.forward_dests(X, [torch.empty((3, 6), device="cuda").data_ptr()], 5, 0)
