@@ -76,6 +76,16 @@ int lmkan_b200_init_table(int n_in, int n_out, int G, uint64_t seed, double init
  * EINVAL if n_in is not a positive even number, n_out <= 0 or G < 3. */
 int lmkan_b200_layer_create(int n_in, int n_out, int G, double gamma, const double* P_host,
                             int device, lmkan_b200_layer** out);
+/* Reference-precision layer: the fp64 table, fp64 weights and fp64
+ * accumulation in the reference's operation order with every operation
+ * explicitly rounded (no FMA contraction), so lmkan_forward's Y is
+ * BIT-IDENTICAL to the reference's (layer.hpp:108-134), for any G >= 3 that
+ * the grid constants hold (<= 64). The forward entry points (device f32/f64,
+ * host f32/f64) and lmkan_b200_layer_read_table accept it; the multi-dest,
+ * conv and model-chain paths return EINVAL. About 2x the shared-memory
+ * traffic of the fp32 gather per coefficient. */
+int lmkan_b200_layer_create_exact(int n_in, int n_out, int G, double gamma, const double* P_host, int device,
+                                  lmkan_b200_layer** out);
 /* Same, from an fp32 table in reference layout already resident on `device`
  * (e.g. generated there); the relayout runs on the device. */
 int lmkan_b200_layer_create_device_f32(int n_in, int n_out, int G, double gamma,
@@ -213,6 +223,7 @@ int lmkan_b200_records_f64(const lmkan_b200_layer* layer, const double* X_dev, i
                            float* ag, int64_t rows, int variant, void* stream);
 
 /* Tuning / introspection: kernel variant chosen for `rows` (OT = output tile,
+ * mode 4 = the reference-precision kernel of an exact layer,
  * RT = rows per thread, NBUF = sheet buffers, rows_per_cta = the row tile,
  * possibly shortened so the grid fills whole waves of SMs), the number of
  * kernel launches one forward issues, the mode (0 = fused locate+gather,

@@ -107,13 +107,17 @@ class Layer:
     # -- construction -------------------------------------------------------
     @classmethod
     def from_host(cls, n_in: int, n_out: int, G: int, P: np.ndarray, gamma: float = 1.0,
-                  device: int = 0) -> "Layer":
+                  device: int = 0, precision: int = 32) -> "Layer":
+        """precision 32: the fp32 gather (1e-5 contract); 64: the
+        reference-precision kernel, bit-identical to the reference forward."""
         P = np.ascontiguousarray(P, dtype=np.float64)
         if P.size != (G + 1) ** 2 * (n_in // 2) * n_out:
             raise ValueError("layer_create: P has the wrong number of coefficients")
+        if precision not in (32, 64):
+            raise ValueError("layer_create: precision must be 32 or 64")
         h = C.c_void_p()
-        check(lib.lmkan_b200_layer_create(int(n_in), int(n_out), int(G), float(gamma), _ptr(P), int(device),
-                                          C.byref(h)))
+        fn = lib.lmkan_b200_layer_create_exact if precision == 64 else lib.lmkan_b200_layer_create
+        check(fn(int(n_in), int(n_out), int(G), float(gamma), _ptr(P), int(device), C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -351,7 +355,7 @@ class Layer:
         d = dict(zip(["out_tile", "rows_per_thread", "nbuf", "rows_per_cta", "launches", "mode", "slabs",
                       "warps_per_cta"],
                      [x.value for x in v]))
-        d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow"}[d["mode"]]
+        d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow", 4: "exact"}[d["mode"]]
         d["lane_vectors"] = int(lib.lmkan_b200_lane_vectors(d["out_tile"]))
         return d
 

@@ -25,6 +25,7 @@ _SIGS = [
     ("lmkan_b200_thresholds", C.c_int, [C.c_int, _P, _P]),
     ("lmkan_b200_init_table", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, _P]),
     ("lmkan_b200_layer_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, _P, C.c_int, C.POINTER(_P)]),
+    ("lmkan_b200_layer_create_exact", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, _P, C.c_int, C.POINTER(_P)]),
     ("lmkan_b200_layer_create_device_f32", C.c_int,
      [C.c_int, C.c_int, C.c_int, C.c_double, _P, C.c_int, C.POINTER(_P)]),
     ("lmkan_b200_layer_create_device_f32_slice", C.c_int,

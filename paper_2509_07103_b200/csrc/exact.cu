@@ -1,0 +1,289 @@
+// Reference-precision forward: lmkan_forward (layer.hpp:108-134) with the fp64
+// table, fp64 weights and fp64 accumulation, every operation explicitly
+// rounded in the reference's order (no FMA contraction), so Y is BIT-IDENTICAL
+// to the reference's lmkan_forward:
+//   weights  w00 = (a c) inv, w10 = (b c) inv, w01 = (a d) inv, w11 = (b d) inv
+//            with a, b, c, d the cell gaps and inv = inv_areas[i1 G + i2]
+//            (grid.hpp:94-100), cells from the fp64 thresholds (bit-exact);
+//   per row  y = 0; for p in order: y += ((w00 p00 + w10 p10) + w01 p01) + w11 p11
+//            (layer.hpp:121-129); y *= gamma (layer.hpp:131).
+// Selected per layer (lmkan_b200_layer_create_exact, the C++ drop-in's
+// LmKanLayer::precision = 64): the fast path stays the fp32 gather
+// (north_star's 1e-5 contract); this one is for callers that need the
+// reference's own numbers (its unit tests compare at 1e-12 .. 1e-14).
+//
+// Kernel: one CTA of 16 warps per (row tile, output tile). The table is laid
+// out [out_tile][pair][node][OT] doubles (OT = 32, 16 or 8 outputs, the widest
+// whose sheet double-buffers in shared memory); per pair the (G+1)^2 x OT
+// sheet arrives by bulk copy (cp.async.bulk + mbarrier, two buffers, a CTA
+// barrier per pair). A warp locates the cells of its rows into a warp-private
+// record slice (fp64 weights), then every lane gathers one output of 32 / OT
+// rows per instruction: LDS.64 of a 256-B (OT = 32) or 128-B (OT = 16) run is
+// 2 wavefronts with no bank conflicts. Sheets too large for shared memory
+// (G > ~40) are read from L2 directly.
+#include <algorithm>
+#include <string>
+
+#include "../../include/lmkan_b200.h"
+#include "layer_impl.hpp"
+
+using namespace lmkan_b200;
+
+namespace {
+
+constexpr int kExactWarps = 16;
+
+// rows per lane group: 32 at OT = 32 (a 512-row tile), 16 at OT = 16 / 8
+constexpr int exact_rt(int OT) { return OT == 32 ? 32 : 16; }
+
+struct ExactSmem {
+    uint32_t sheet_bytes, off_recw, off_recn, off_thr, off_pts, off_bar, total;
+};
+__host__ __device__ inline ExactSmem exact_smem_layout(int G, int OT, bool gsheet) {
+    const int rows_w = (32 / OT) * exact_rt(OT);
+    ExactSmem s;
+    s.sheet_bytes = (static_cast<uint32_t>((G + 1) * (G + 1)) * OT * 8u + 127u) & ~127u;
+    uint32_t o = gsheet ? 0u : 2u * s.sheet_bytes;
+    s.off_recw = o;
+    o += kExactWarps * rows_w * 32u;  // double4 weights
+    s.off_recn = o;
+    o += kExactWarps * rows_w * 4u;  // node index
+    o = (o + 15u) & ~15u;
+    s.off_thr = o;
+    o += kMaxThr * 8u;
+    s.off_pts = o;
+    o += (kMaxThr + 1) * 8u;
+    o = (o + 15u) & ~15u;
+    s.off_bar = o;
+    o += 16u;
+    s.total = (o + 127u) & ~127u;
+    return s;
+}
+
+template <int OT, typename XT, bool GSHEET>
+__global__ void __launch_bounds__(kExactWarps * 32, 1)
+    exact_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
+                 const double* __restrict__ table, int pairs, double gamma, const __grid_constant__ GridConst gc) {
+    constexpr int RT = exact_rt(OT), RPI = 32 / OT, ROWS_W = RPI * RT, LOC = (ROWS_W + 31) / 32;
+    constexpr int R = kExactWarps * ROWS_W;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int G = gc.G, nodes = (G + 1) * (G + 1);
+    const ExactSmem Ls = exact_smem_layout(G, OT, GSHEET);
+    double* sheets = reinterpret_cast<double*>(smem);
+    double4* recw = reinterpret_cast<double4*>(smem + Ls.off_recw);
+    int* recn = reinterpret_cast<int*>(smem + Ls.off_recn);
+    double* thr = reinterpret_cast<double*>(smem + Ls.off_thr);
+    double* pts = reinterpret_cast<double*>(smem + Ls.off_pts);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Ls.off_bar);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int k = tid; k < kMaxThr; k += kExactWarps * 32) thr[k] = gc.t64[k];
+    for (int k = tid; k <= G; k += kExactWarps * 32) pts[k] = gc.points[k];
+    const int ot = blockIdx.y;
+    const double* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;
+    const uint32_t sheet_copy = static_cast<uint32_t>(nodes) * OT * 8u;
+    uint64_t policy = 0;
+    auto issue = [&](int p) {  // thread 0: sheet of pair p into buffer p & 1
+        mbar_arrive_expect_tx(&bar[p & 1], sheet_copy);
+        const char* src = reinterpret_cast<const char*>(tsrc + static_cast<size_t>(p) * nodes * OT);
+        char* dst = reinterpret_cast<char*>(sheets) + (p & 1) * Ls.sheet_bytes;
+        for (uint32_t o = 0; o < sheet_copy; o += 32768u)
+            bulk_g2s(dst + o, src + o, sheet_copy - o < 32768u ? sheet_copy - o : 32768u, &bar[p & 1], policy);
+    };
+    if constexpr (!GSHEET) {
+        if (tid == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            fence_barrier_init();
+            policy = policy_evict_last();
+            issue(0);
+            if (pairs > 1) issue(1);
+        }
+    }
+    __syncthreads();
+
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * R + warp * ROWS_W;
+    const int g = lane / OT, o = lane % OT;
+    const int col = ot * OT + o;
+    double4* wrec = recw + warp * ROWS_W;
+    int* nrec = recn + warp * ROWS_W;
+    double acc[RT];
+#pragma unroll
+    for (int j = 0; j < RT; ++j) acc[j] = 0.0;
+
+    for (int p = 0; p < pairs; ++p) {
+        // cells of the warp's rows for pair p (lane: rows q = k*32 + lane)
+#pragma unroll
+        for (int k = 0; k < LOC; ++k) {
+            const int q = k * 32 + lane;
+            if (q < ROWS_W) {
+                const int64_t r = row0 + q;
+                double4 w = make_double4(0.0, 0.0, 0.0, 0.0);
+                int node = 0;
+                if (r < rows) {
+                    const double x1 = static_cast<double>(X[r * n_in + 2 * p]);
+                    const double x2 = static_cast<double>(X[r * n_in + 2 * p + 1]);
+                    const int i1 = cell_index<double>(x1, thr, gc.L), i2 = cell_index<double>(x2, thr, gc.L);
+                    const double a = __dsub_rn(pts[i1 + 1], x1), b = __dsub_rn(x1, pts[i1]);
+                    const double c = __dsub_rn(pts[i2 + 1], x2), d = __dsub_rn(x2, pts[i2]);
+                    const double inv = __ldg(gc.inv_areas + i1 * G + i2);
+                    w = make_double4(__dmul_rn(__dmul_rn(a, c), inv), __dmul_rn(__dmul_rn(b, c), inv),
+                                     __dmul_rn(__dmul_rn(a, d), inv), __dmul_rn(__dmul_rn(b, d), inv));
+                    node = i1 * (G + 1) + i2;
+                }
+                wrec[q] = w;
+                nrec[q] = node;
+            }
+        }
+        __syncwarp();
+        const double* sh;
+        if constexpr (GSHEET) {
+            sh = tsrc + static_cast<size_t>(p) * nodes * OT;
+        } else {
+            mbar_wait(&bar[p & 1], static_cast<uint32_t>((p >> 1) & 1));
+            sh = sheets + (p & 1) * (Ls.sheet_bytes / 8);
+        }
+#pragma unroll
+        for (int j = 0; j < RT; ++j) {
+            const int q = j * RPI + g;
+            const double4 w = wrec[q];
+            const double* b0 = sh + nrec[q] * OT + o;
+            const double* b1 = b0 + (G + 1) * OT;
+            double p00, p10, p01, p11;
+            if constexpr (GSHEET) {
+                p00 = __ldg(b0), p10 = __ldg(b1), p01 = __ldg(b0 + OT), p11 = __ldg(b1 + OT);
+            } else {
+                p00 = b0[0], p10 = b1[0], p01 = b0[OT], p11 = b1[OT];
+            }
+            const double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w.x, p00), __dmul_rn(w.y, p10)),
+                                                 __dmul_rn(w.z, p01)),
+                                       __dmul_rn(w.w, p11));
+            acc[j] = __dadd_rn(acc[j], t);
+        }
+        __syncthreads();  // every warp is done with buffer p & 1 and with its records
+        if constexpr (!GSHEET) {
+            if (tid == 0 && p + 2 < pairs) {
+                fence_proxy_async();
+                issue(p + 2);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < RT; ++j) {
+        const int64_t r = row0 + j * RPI + g;
+        if (r < rows && col < n_out) Y[r * n_out + col] = static_cast<XT>(__dmul_rn(acc[j], gamma));
+    }
+}
+
+// Reference layout src[node][pair][n_out] (doubles) -> [ot][pair][node][OT].
+__global__ void relayout64_kernel(const double* __restrict__ src, double* __restrict__ dst, int pairs, int nodes,
+                                  int n_out, int OT, int n_ot) {
+    const size_t total = static_cast<size_t>(n_ot) * pairs * nodes * OT;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int qq = static_cast<int>(i % OT);
+        size_t t = i / OT;
+        const int node = static_cast<int>(t % nodes);
+        t /= nodes;
+        const int p = static_cast<int>(t % pairs);
+        const int q = static_cast<int>(t / pairs) * OT + qq;
+        dst[i] = q < n_out ? src[(static_cast<size_t>(node) * pairs + p) * n_out + q] : 0.0;
+    }
+}
+
+__global__ void export64_kernel(const double* __restrict__ table, double* __restrict__ dst, int pairs, int nodes,
+                                int n_out, int OT, int pb, int pe) {
+    const int np = pe - pb;
+    const size_t total = static_cast<size_t>(nodes) * np * n_out;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int q = static_cast<int>(i % n_out);
+        size_t t = i / n_out;
+        const int pl = static_cast<int>(t % np);
+        const int node = static_cast<int>(t / np);
+        dst[i] = table[((static_cast<size_t>(q / OT) * pairs + pb + pl) * nodes + node) * OT + q % OT];
+    }
+}
+
+unsigned blocks_for(size_t total) { return static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 64)); }
+
+template <int OT, typename XT, bool GS>
+cudaError_t launch_exact_t(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+    constexpr int R = kExactWarps * (32 / OT) * exact_rt(OT);
+    auto kern = exact_kernel<OT, XT, GS>;
+    const uint32_t smem = exact_smem_layout(L->G, OT, GS).total;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t tiles = (rows + R - 1) / R;
+    dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(L->n_ot));
+    kern<<<grid, kExactWarps * 32, smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table64, L->pairs, L->gamma, L->gc);
+    return cudaGetLastError();
+}
+
+template <typename XT>
+cudaError_t launch_exact(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+    const bool gs = L->exact_gsheet;
+    switch (L->OT) {
+        case 32: return gs ? launch_exact_t<32, XT, true>(L, X, Y, rows, st) : launch_exact_t<32, XT, false>(L, X, Y, rows, st);
+        case 16: return gs ? launch_exact_t<16, XT, true>(L, X, Y, rows, st) : launch_exact_t<16, XT, false>(L, X, Y, rows, st);
+        default: return gs ? launch_exact_t<8, XT, true>(L, X, Y, rows, st) : launch_exact_t<8, XT, false>(L, X, Y, rows, st);
+    }
+}
+
+}  // namespace
+
+namespace lmkan_b200::api {
+
+// Output tile of a reference-precision layer: the widest of {32, 16, 8}
+// doubles whose sheet double-buffers in shared memory next to the records;
+// else 8 with sheets read from L2 (gsheet).
+void exact_choose(int n_out, int G, int smem_cap, int& OT, bool& gsheet) {
+    for (int ot : {32, 16, 8}) {
+        if (ot > 8 && ot / 2 >= n_out) continue;  // do not pad a narrow layer by 2x
+        if (static_cast<int>(exact_smem_layout(G, ot, false).total) <= smem_cap) {
+            OT = ot;
+            gsheet = false;
+            return;
+        }
+    }
+    OT = 8;
+    gsheet = true;
+}
+
+int exact_upload(lmkan_b200_layer* L, const double* P_host) {
+    const size_t count = static_cast<size_t>(L->nodes) * L->pairs * L->n_out;
+    double* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, count * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(tmp, P_host, count * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const size_t total = L->table64_bytes / sizeof(double);
+        relayout64_kernel<<<blocks_for(total), 256>>>(tmp, L->table64, L->pairs, L->nodes, L->n_out, L->OT, L->n_ot);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    return e == cudaSuccess ? LMKAN_B200_OK : cuda_error(e, "layer_create_exact: upload P");
+}
+
+int exact_read_table(const lmkan_b200_layer* L, int pb, int pe, double* dst_host) {
+    const size_t count = static_cast<size_t>(L->nodes) * (pe - pb) * L->n_out;
+    double* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, count * sizeof(double));
+    if (e == cudaSuccess) {
+        export64_kernel<<<blocks_for(count), 256>>>(L->table64, tmp, L->pairs, L->nodes, L->n_out, L->OT, pb, pe);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(dst_host, tmp, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    return e == cudaSuccess ? LMKAN_B200_OK : cuda_error(e, "read_table");
+}
+
+int forward_exact(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, cudaStream_t st) {
+    const cudaError_t e = launch_exact<float>(L, X, Y, rows, st);
+    return e == cudaSuccess ? LMKAN_B200_OK : cuda_error(e, "lmkan_forward: exact kernel launch");
+}
+int forward_exact(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st) {
+    const cudaError_t e = launch_exact<double>(L, X, Y, rows, st);
+    return e == cudaSuccess ? LMKAN_B200_OK : cuda_error(e, "lmkan_forward: exact kernel launch");
+}
+
+}  // namespace lmkan_b200::api

@@ -19,6 +19,13 @@ struct lmkan_b200_layer {
     int ns = 64;          // node stride of the device table in floats (OT, or 2 OT when dup)
     int pair_block = 0;   // pair-block summation block (0: one running sum; see fwd_fused_kernel)
     int num_sms = 148;    // the device's SM count (queried at creation)
+    // reference precision (lmkan_b200_layer_create_exact): fp64 table
+    // [out_tile][pair][node][OT] (OT = 32 / 16 / 8 doubles) and the exact kernel
+    // (csrc/exact.cu); no fp32 table
+    bool exact = false;
+    bool exact_gsheet = false;  // sheets read from L2 (too large for shared memory)
+    double* table64 = nullptr;
+    size_t table64_bytes = 0;
     float* table = nullptr;
     size_t table_bytes = 0;
     double* d_inv = nullptr;
@@ -64,6 +71,12 @@ int forward_device(const lmkan_b200_layer* L, const float* X, float* Y, int64_t 
 int forward_chain_f32(const lmkan_b200_layer* const* layers, int n, const float* X, float* Y, int64_t rows,
                       void* const* acts, cudaStream_t st);
 int forward_device(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st);
+// reference-precision layers (csrc/exact.cu)
+void exact_choose(int n_out, int G, int smem_cap, int& OT, bool& gsheet);
+int exact_upload(lmkan_b200_layer* L, const double* P_host);
+int exact_read_table(const lmkan_b200_layer* L, int pair_begin, int pair_end, double* dst_host);
+int forward_exact(const lmkan_b200_layer* L, const float* X, float* Y, int64_t rows, cudaStream_t st);
+int forward_exact(const lmkan_b200_layer* L, const double* X, double* Y, int64_t rows, cudaStream_t st);
 }  // namespace api
 
 }  // namespace lmkan_b200

@@ -413,6 +413,11 @@ int forward_device_dests(const lmkan_b200_layer* L, const XT* X, const OutDests<
     if (out.col0 < 0 || out.ld < out.col0 + L->n_out)
         return fail(LMKAN_B200_EINVAL, "lmkan_forward: output row stride narrower than the layer's columns");
     DeviceGuard g(L->device);
+    if (L->exact) {  // reference precision: plain [rows][n_out] output only
+        if (out.n != 1 || out.col0 != 0 || out.ld != L->n_out || im.conv)
+            return fail(LMKAN_B200_EINVAL, "lmkan_forward: reference-precision layers support the plain forward only");
+        return api::forward_exact(L, X, out.base[0], rows, st);
+    }
     const int cap = max_smem_optin(L->device);
     Plan pl;
     if (!make_plan(L, rows, cap, pl))
@@ -475,6 +480,7 @@ int records_device(const lmkan_b200_layer* L, const XT* X, int32_t* i1, int32_t*
         return fail(LMKAN_B200_EINVAL, "records: null or misaligned output");
     if (variant < 0 || variant > 2) return fail(LMKAN_B200_EINVAL, "records: variant must be 0, 1 or 2");
     if (variant < 2 && L->narrow) return fail(LMKAN_B200_EINVAL, "records: narrow layers have no K1 records");
+    if (L->exact) return fail(LMKAN_B200_EINVAL, "records: reference-precision layers keep fp64 records in-kernel");
     DeviceGuard g(L->device);
     const int cap = max_smem_optin(L->device);
     const int64_t total = rows * L->pairs;
@@ -526,7 +532,7 @@ int validate_shape(int n_in, int n_out, int G) {
 
 // Allocates the handle, grid constants and the (uninitialised) device table.
 int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G, double gamma, int device,
-                lmkan_b200_layer** out) {
+                lmkan_b200_layer** out, bool exact = false) {
     if (!out) return fail(LMKAN_B200_EINVAL, "layer_create: null out pointer");
     *out = nullptr;
     if (int rc = validate_shape(n_in, n_out_total, G)) return rc;
@@ -550,7 +556,10 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
             L->num_sms = sms;
     }
     const int no = n_out_local <= 1 ? 1 : (n_out_local <= 2 ? 2 : 4);
-    if (n_out_local <= 4 && env_int("LMKAN_B200_NARROW", 1) &&
+    if (exact) {
+        L->exact = true;
+        api::exact_choose(n_out_local, G, max_smem_optin(device), L->OT, L->exact_gsheet);
+    } else if (n_out_local <= 4 && env_int("LMKAN_B200_NARROW", 1) &&
         static_cast<int>(narrow_smem_bytes(G, n_in / 2, no)) <= max_smem_optin(device)) {
         L->narrow = true;
         L->OT = no;
@@ -577,18 +586,22 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     }
     for (int k = 0; k <= kMaxThr; ++k) gc.points[k] = k <= G ? pts[k] : 0.0;
     for (int k = 0; k < kMaxThr; ++k) gc.inv_h[k] = k < G ? 1.0 / (pts[k + 1] - pts[k]) : 0.0;
-    L->table_bytes = static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->ns * sizeof(float);
+    L->table_bytes = exact ? 0 : static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->ns * sizeof(float);
+    L->table64_bytes = exact ? static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->OT * sizeof(double) : 0;
     cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
     if (e == cudaSuccess)
         e = cudaMemcpy(L->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice);
     // the allocation is rounded up to 16 B and the tail zeroed: the narrow kernel
     // bulk-copies the whole table, and bulk copies move multiples of 16 B
     const size_t alloc_bytes = (L->table_bytes + 15) & ~static_cast<size_t>(15);
-    if (e == cudaSuccess) e = cudaMalloc(&L->table, alloc_bytes);
-    if (e == cudaSuccess && alloc_bytes > L->table_bytes)
+    if (e == cudaSuccess && exact) e = cudaMalloc(&L->table64, L->table64_bytes);
+    if (e == cudaSuccess && !exact) e = cudaMalloc(&L->table, alloc_bytes);
+    if (e == cudaSuccess && !exact && alloc_bytes > L->table_bytes)
         e = cudaMemset(reinterpret_cast<char*>(L->table) + L->table_bytes, 0, alloc_bytes - L->table_bytes);
     if (e != cudaSuccess) {
         cudaFree(L->d_inv);
+        cudaFree(L->table64);
+        cudaFree(L->table);
         delete L;
         return cuda_fail(e, "layer_create: device allocation");
     }
@@ -655,7 +668,7 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     // fp64 callers: Y crosses PCIe as fp32 (exact: every output is an fp32 sum
     // times an fp32 gamma) and is widened on the host; the slot's device Y holds
     // [fp32 Y | fp64 Y]
-    const bool widen = sizeof(XT) == 8 && env_int("LMKAN_B200_HOST_F32_Y", 1) != 0;
+    const bool widen = sizeof(XT) == 8 && !L->exact && env_int("LMKAN_B200_HOST_F32_Y", 1) != 0;
     const size_t y32_bytes = (static_cast<size_t>(chunk) * L->n_out * sizeof(float) + 255) & ~static_cast<size_t>(255);
     CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT),
                  static_cast<size_t>(chunk) * L->n_out * sizeof(XT) + (widen ? y32_bytes : 0)));
@@ -856,6 +869,19 @@ int lmkan_b200_layer_create(int n_in, int n_out, int G, double gamma, const doub
     return rc;
 }
 
+int lmkan_b200_layer_create_exact(int n_in, int n_out, int G, double gamma, const double* P_host, int device,
+                                  lmkan_b200_layer** out) {
+    if (!P_host) return fail(LMKAN_B200_EINVAL, "layer_create: null P");
+    if (int rc = alloc_layer(n_in, n_out, n_out, 0, G, gamma, device, out, true)) return rc;
+    DeviceGuard g(device);
+    const int rc = api::exact_upload(*out, P_host);
+    if (rc) {
+        lmkan_b200_layer_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
 int lmkan_b200_layer_create_device_f32_slice(int n_in, int n_out, int G, double gamma, const float* P_dev,
                                              int out_begin, int out_end, int device, lmkan_b200_layer** out) {
     if (!P_dev) return fail(LMKAN_B200_EINVAL, "layer_create: null P");
@@ -897,6 +923,7 @@ int lmkan_b200_layer_read_table(const lmkan_b200_layer* L, int pair_begin, int p
     if (pair_begin < 0 || pair_end > L->pairs || pair_begin >= pair_end)
         return fail(LMKAN_B200_EINVAL, "read_table: bad pair range");
     DeviceGuard g(L->device);
+    if (L->exact) return api::exact_read_table(L, pair_begin, pair_end, dst);
     const size_t count = static_cast<size_t>(L->nodes) * (pair_end - pair_begin) * L->n_out;
     double* tmp = nullptr;
     CK(cudaMalloc(&tmp, count * sizeof(double)));
@@ -933,6 +960,7 @@ int lmkan_b200_layer_destroy(lmkan_b200_layer* L) {
     {
         DeviceGuard g(L->device);
         cudaFree(L->table);
+        cudaFree(L->table64);
         cudaFree(L->d_inv);
     }
     delete L;
@@ -1125,6 +1153,17 @@ int lmkan_b200_lane_vectors(int out_tile) { return lane_vectors(out_tile); }
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
                     int* rows_per_cta_out, int* launches, int* mode, int* slabs, int* warps_per_cta) {
     if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
+    if (L->exact) {  // mode 4: the reference-precision kernel (one launch, 16 warps per CTA)
+        if (out_tile) *out_tile = L->OT;
+        if (rows_per_thread) *rows_per_thread = L->OT == 32 ? 32 : 16;
+        if (nbuf) *nbuf = L->exact_gsheet ? 0 : 2;
+        if (rows_per_cta_out) *rows_per_cta_out = 16 * (32 / L->OT) * (L->OT == 32 ? 32 : 16);
+        if (launches) *launches = 1;
+        if (mode) *mode = 4;
+        if (slabs) *slabs = 1;
+        if (warps_per_cta) *warps_per_cta = 16;
+        return LMKAN_B200_OK;
+    }
     Plan pl;
     if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits");
     if (out_tile) *out_tile = pl.OT;

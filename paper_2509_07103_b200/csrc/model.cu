@@ -715,6 +715,8 @@ int lmkan_b200_model_create(lmkan_b200_layer* const* layers, int n_layers, lmkan
     int dev0 = -1;
     for (int i = 0; i < n_layers; ++i) {
         if (!layers[i]) return api::set_error(LMKAN_B200_EINVAL, "model_create: null layer");
+        if (layers[i]->exact)
+            return api::set_error(LMKAN_B200_EINVAL, "model_create: reference-precision layers are not chained on the device");
         int d = 0;
         lmkan_b200_layer_info(layers[i], nullptr, nullptr, nullptr, &d, nullptr, nullptr);
         if (dev0 >= 0 && d != dev0) return api::set_error(LMKAN_B200_EINVAL, "model_create: layers on different devices");
