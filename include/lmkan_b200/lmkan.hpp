@@ -33,8 +33,10 @@
 #include <cstring>
 #include <initializer_list>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -114,6 +116,13 @@ inline double sigma(double x) {
     return x > 0.0 ? 1.0 - 0.5 * t : 0.5 * t;
 }
 
+// grid.hpp:20-24: analytic inverse of sigma on (0, 1); std::domain_error outside.
+inline double sigma_inv(double p) {
+    if (!(p > 0.0 && p < 1.0)) throw std::domain_error("sigma_inv: p must lie in (0, 1)");
+    if (p > 0.5) return -std::log(2.0 * (1.0 - p));
+    return std::log(2.0 * p);
+}
+
 // grid.hpp:72-75, bit-exact: #{k : x >= t_k} (NaN -> 0).
 inline int interval_index(const SigmaGrid& grid, double x) {
     int i = 0;
@@ -142,6 +151,98 @@ inline Preamble preamble(const SigmaGrid& grid, double x1, double x2) {
     r.w11 = b * d * inv;
     return r;
 }
+
+// rng.hpp:19-79: the reference's named random stream, reproduced bit for bit
+// (the same keying, engine and transforms) so data drawn by existing callers
+// and tests is unchanged: key = splitmix64 finalizer of seed ^ (FNV-1a(name) +
+// golden ratio), engine std::mt19937_64(key), uniforms from the top 53 bits,
+// normals by Box-Muller returning the cosine half first and caching the sine.
+class RandomStream {
+public:
+    RandomStream(std::uint64_t seed, std::string_view name) : key_(derive(seed, name)), eng_(key_) {}
+    RandomStream split(std::string_view child) const { return RandomStream(key_, child); }
+    std::uint64_t next_u64() { return eng_(); }
+    double uniform() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
+    double uniform_open() {
+        double u = uniform();
+        while (u == 0.0) u = uniform();
+        return u;
+    }
+    double normal() {
+        if (have_) {
+            have_ = false;
+            return spare_;
+        }
+        const double u1 = uniform_open(), u2 = uniform();
+        const double rad = std::sqrt(-2.0 * std::log(u1)), ang = 2.0 * M_PI * u2;
+        spare_ = rad * std::sin(ang);
+        have_ = true;
+        return rad * std::cos(ang);
+    }
+
+private:
+    static std::uint64_t derive(std::uint64_t seed, std::string_view name) {
+        std::uint64_t h = 0xcbf29ce484222325ull;
+        for (unsigned char ch : name) h = (h ^ ch) * 0x100000001b3ull;
+        std::uint64_t z = seed ^ (h + 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    std::uint64_t key_;
+    std::mt19937_64 eng_;
+    bool have_ = false;
+    double spare_ = 0.0;
+};
+
+// func2d.hpp:14-24: one 2D function as its (G+1) x (G+1) node coefficients,
+// row-major [i1 (G+1) + i2] (indices 0 and G sit on the ghost points).
+struct Func2D {
+    int G = 0;
+    std::vector<double> coeffs;
+    Func2D() = default;
+    explicit Func2D(int G_, double fill = 0.0) : G(G_), coeffs(static_cast<std::size_t>(G_ + 1) * (G_ + 1), fill) {}
+    double& at(int i1, int i2) { return coeffs[static_cast<std::size_t>(i1) * (G + 1) + i2]; }
+    double at(int i1, int i2) const { return coeffs[static_cast<std::size_t>(i1) * (G + 1) + i2]; }
+};
+
+// func2d.hpp:26-48: the 1D hat basis function i in [0, G] at x, evaluated from
+// the grid points alone (1 at points[i], 0 at its neighbours); the hats of the
+// two unbounded edge intervals keep their slope out to +-infinity, as the
+// ghost-point extrapolation of the lookup does.
+inline double basis_weight_1d(const SigmaGrid& grid, int i, double x) {
+    const int G = grid.G;
+    if (i < 0 || i > G) throw std::out_of_range("basis_weight_1d: index outside [0, G]");
+    const std::vector<double>& t = grid.points;
+    const bool left_open = i == 1, right_open = i == G - 1;
+    if (i == 0) return x < t[1] ? (t[1] - x) / (t[1] - t[0]) : 0.0;
+    if (i == G) return x > t[G - 1] ? (x - t[G - 1]) / (t[G] - t[G - 1]) : 0.0;
+    if (x < t[i]) return (left_open || x >= t[i - 1]) ? (x - t[i - 1]) / (t[i] - t[i - 1]) : 0.0;
+    return (right_open || x <= t[i + 1]) ? (t[i + 1] - x) / (t[i + 1] - t[i]) : 0.0;
+}
+
+// func2d.hpp:50-57: the O(1) bilinear lookup of one 2D function.
+inline double eval2d(const SigmaGrid& grid, const Func2D& f, double x1, double x2);
+
+// func2d.hpp:62-73: the dense O(G^2) basis-product sum eval2d must equal.
+inline double eval2d_dense_oracle(const SigmaGrid& grid, const Func2D& f, double x1, double x2) {
+    double sum = 0.0;
+    for (int i1 = 0; i1 <= grid.G; ++i1) {
+        const double u = basis_weight_1d(grid, i1, x1);
+        if (u == 0.0) continue;
+        for (int i2 = 0; i2 <= grid.G; ++i2) sum += f.at(i1, i2) * u * basis_weight_1d(grid, i2, x2);
+    }
+    return sum;
+}
+
+// func2d.hpp:75-105: input derivatives of the bilinear cell form and the four
+// coefficient weights of the active cell.
+struct Grad2D {
+    double df_dx1 = 0, df_dx2 = 0;
+    int i1 = 0, i2 = 0;
+    double w00 = 0, w10 = 0, w01 = 0, w11 = 0;
+};
+inline Grad2D grad2d(const SigmaGrid& grid, const Func2D& f, double x1, double x2);
 
 // std::vector<double> with a mutation generation, the type of LmKanLayer::P.
 // Every non-const access (element references, data(), iterators, assign /
@@ -232,6 +333,32 @@ private:
     std::uint64_t gen_ = 0;
 };
 
+inline double eval2d(const SigmaGrid& grid, const Func2D& f, double x1, double x2) {
+    const Preamble c = preamble(grid, x1, x2);
+    const std::size_t row = static_cast<std::size_t>(grid.G) + 1, n = c.i1 * row + c.i2;
+    const double* k = f.coeffs.data();
+    return c.w00 * k[n] + c.w01 * k[n + 1] + c.w10 * k[n + row] + c.w11 * k[n + row + 1];
+}
+
+inline Grad2D grad2d(const SigmaGrid& grid, const Func2D& f, double x1, double x2) {
+    const Preamble c = preamble(grid, x1, x2);
+    Grad2D g;
+    g.i1 = c.i1;
+    g.i2 = c.i2;
+    g.w00 = c.w00;
+    g.w10 = c.w10;
+    g.w01 = c.w01;
+    g.w11 = c.w11;
+    const double f00 = f.at(c.i1, c.i2), f10 = f.at(c.i1 + 1, c.i2);
+    const double f01 = f.at(c.i1, c.i2 + 1), f11 = f.at(c.i1 + 1, c.i2 + 1);
+    const double inv = grid.inv_area(c.i1, c.i2);
+    const double lo1 = grid.points[c.i1], hi1 = grid.points[c.i1 + 1];
+    const double lo2 = grid.points[c.i2], hi2 = grid.points[c.i2 + 1];
+    g.df_dx1 = ((f10 - f00) * (hi2 - x2) + (f11 - f01) * (x2 - lo2)) * inv;
+    g.df_dx2 = ((f01 - f00) * (hi1 - x1) + (f11 - f10) * (x1 - lo1)) * inv;
+    return g;
+}
+
 namespace detail {
 struct Prepared {
     lmkan_b200_layer* h = nullptr;
@@ -239,11 +366,23 @@ struct Prepared {
     const double* data = nullptr;
     std::size_t size = 0;
     std::uint64_t generation = 0;
+    int precision = 32;
     ~Prepared() {
         if (h) lmkan_b200_layer_destroy(h);
     }
 };
 }  // namespace detail
+
+// Arithmetic of a layer's device forward: 32 = the fp32 gather (the product
+// path, |y - y_ref| <= 1e-5 max(1, |y_ref|)); 64 = reference precision, Y
+// bit-identical to the reference's lmkan_forward (lmkan_b200_layer_create_exact).
+// New layers take LMKAN_B200_PRECISION (32 / 64 / fp32 / fp64), default 32.
+inline int default_precision() {
+    const char* e = std::getenv("LMKAN_B200_PRECISION");
+    if (!e) return 32;
+    const std::string v(e);
+    return (v == "64" || v == "fp64" || v == "f64") ? 64 : 32;
+}
 
 // layer.hpp:24-61. Same public fields and the same P layout
 // [i1][i2][pair][out] (out fastest); `device` selects the GPU.
@@ -254,15 +393,18 @@ struct LmKanLayer {
     ParamVector P;  // std::vector<double> semantics; tracks modifications (see ParamVector)
     double gamma = 0.0;
     int device = 0;
+    int precision = default_precision();  // 32 or 64, see default_precision
 
     LmKanLayer() = default;
     // Copies share no device state: a copied layer (whose P the caller may then
     // edit) prepares its own table on first use.
     LmKanLayer(const LmKanLayer& o)
-        : n_in(o.n_in), n_out(o.n_out), grid(o.grid), P(o.P), gamma(o.gamma), device(o.device) {}
+        : n_in(o.n_in), n_out(o.n_out), grid(o.grid), P(o.P), gamma(o.gamma), device(o.device),
+          precision(o.precision) {}
     LmKanLayer& operator=(const LmKanLayer& o) {
         if (this != &o) {
             n_in = o.n_in; n_out = o.n_out; grid = o.grid; P = o.P; gamma = o.gamma; device = o.device;
+            precision = o.precision;
             cache_.reset();
         }
         return *this;
@@ -283,6 +425,20 @@ struct LmKanLayer {
         return P.data() + node_offset(i1, i2) + static_cast<std::size_t>(pair) * n_out;
     }
 
+    // layer.hpp:47-60: one function's (pair, out) coefficient sheet as a Func2D, and back.
+    Func2D sheet(int pair, int out) const {
+        Func2D f(grid.G);
+        for (int i1 = 0; i1 <= grid.G; ++i1)
+            for (int i2 = 0; i2 <= grid.G; ++i2) f.at(i1, i2) = node_slice(i1, i2, pair)[out];
+        return f;
+    }
+    void set_sheet(int pair, int out, const Func2D& f) {
+        double* base = P.data();  // one generation bump for the whole sheet
+        for (int i1 = 0; i1 <= grid.G; ++i1)
+            for (int i2 = 0; i2 <= grid.G; ++i2)
+                base[node_offset(i1, i2) + static_cast<std::size_t>(pair) * n_out + out] = f.at(i1, i2);
+    }
+
     // Drop the device table (e.g. to free GPU memory); rebuilt on next use.
     void release() const { cache_.reset(); }
 
@@ -291,10 +447,15 @@ struct LmKanLayer {
     lmkan_b200_layer* prepared() const {
         if (!cache_ || cache_->generation != P.generation() || cache_->data != P.data() ||
             cache_->size != P.size() || cache_->n_in != n_in || cache_->n_out != n_out ||
-            cache_->G != grid.G || cache_->device != device) {
+            cache_->G != grid.G || cache_->device != device || cache_->precision != precision) {
             auto pr = std::make_shared<detail::Prepared>();
-            detail::throw_status(
-                lmkan_b200_layer_create(n_in, n_out, grid.G, gamma, P.data(), device, &pr->h), "lmkan_forward");
+            if (precision == 64)
+                detail::throw_status(
+                    lmkan_b200_layer_create_exact(n_in, n_out, grid.G, gamma, P.data(), device, &pr->h), "lmkan_forward");
+            else
+                detail::throw_status(
+                    lmkan_b200_layer_create(n_in, n_out, grid.G, gamma, P.data(), device, &pr->h), "lmkan_forward");
+            pr->precision = precision;
             pr->n_in = n_in; pr->n_out = n_out; pr->G = grid.G; pr->device = device;
             pr->data = P.data();
             pr->size = P.size();
