@@ -268,6 +268,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--precision", type=int, default=32, choices=[32, 64],
+                    help="64: reference-precision layers (fp64 table and accumulation, bit-identical to the "
+                         "reference forward; single dense layers only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
@@ -323,6 +326,14 @@ def main():
         # all-gather of the column shards: fused into the gather kernel's
         # epilogue (NVLink stores into every rank's Y + device barrier), or NCCL
         peers = sharding.PeerGather(B, n_out0, local) if ws > 1 and args.gather == "fused" else None
+    elif args.precision == 64:
+        if len(cfg["layers"]) != 1 or cfg.get("conv"):
+            raise SystemExit("--precision 64: single dense layer configs only (1, 2)")
+        n_in, n_out = cfg["layers"][0]
+        rng = np.random.default_rng(1000)
+        P = rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)
+        layers = [pkg.Layer.from_host(n_in, n_out, G, P, 1.0, device=local, precision=64)]
+        del P
     else:
         layers = [pkg.Layer.random(n_in, n_out, G, seed=1000 + i, gamma=1.0, device=local)
                   for i, (n_in, n_out) in enumerate(cfg["layers"])]
@@ -341,7 +352,7 @@ def main():
     # Chains (and launch-bound tiny batches) run through the model API: one
     # device chain per step, replayed from a CUDA graph (needs a non-legacy
     # stream); single wide layers launch directly on the current stream.
-    use_model = not conv and not out_sharded and (len(layers) > 1 or bool(cfg.get("small")))
+    use_model = not conv and not out_sharded and args.precision == 32 and (len(layers) > 1 or bool(cfg.get("small")))
     model = pkg.Model.from_layers(layers) if use_model else None
     stream = torch.cuda.Stream() if use_model else torch.cuda.current_stream()
     K = args.steps
@@ -488,7 +499,8 @@ def main():
         n_in0, n_out0 = cfg["layers"][0]
         Kd = max(3, min(K, 10))
         r = subprocess.run([dropin_bin, str(n_in0), str(n_out0), str(G), str(B), str(Kd), "2", str(local)],
-                           capture_output=True, text=True, timeout=900)
+                           capture_output=True, text=True, timeout=900,
+                           env={**os.environ, "LMKAN_B200_PRECISION": str(args.precision)})
         if r.returncode == 0:
             d = json.loads(r.stdout.strip().splitlines()[-1])
             td = torch.tensor([d["ms_per_step"]], device=f"cuda:{local}")
@@ -512,10 +524,12 @@ def main():
     clocks = sampler.summary()
     peak, peak_src = load_peaks()
     balg_row = sum(b_alg(a, b) for a, b in cfg["layers"])
+    if args.precision == 64:  # 8-byte coefficients and I/O
+        balg_row = sum(2 * b_alg(a, b) for a, b in cfg["layers"])
     achieved = B * balg_row / (kernel_ms / 1e3) / 1e9
     plan = layers[0].plan(B)
     cpu = None
-    if not args.no_cpu_baseline and ws == 1:
+    if not args.no_cpu_baseline and ws == 1 and args.precision == 32:
         if out_sharded:  # 146 GB fp64 table does not fit the host: time a 16-output slice, scale by cost ~ n_out
             n_in0 = cfg["layers"][0][0]
             sl = pkg.Layer.random(n_in0, n_out0, G, seed=1000, gamma=1.0, device=local, out_range=(0, 16))
@@ -543,7 +557,9 @@ def main():
         "higher_is_better": True,
         "scaling": "strong" if out_sharded else "weak",
         "vs_baseline": None,
-        "dtype": "fp32",
+        "dtype": "fp64" if args.precision == 64 else "fp32",
+        "precision": ("reference (fp64 table and accumulation, bit-identical to the reference forward)"
+                      if args.precision == 64 else "fp32 gather (|y - y_ref| <= 1e-5 max(1, |y_ref|))"),
         "data": "synthetic: X ~ N(0,1) (torch CUDA generator), table ~ N(0, 1/pairs) from a device counter RNG",
         "config": config_dict(CONFIGS[args.config], ws, rank, shards, args.gather),
         "kernel_plan": dict(plan, n_out_local=cfg["layers"][0][1]),
@@ -563,7 +579,8 @@ def main():
                      "fp32_fma_tflops": fmas / (kernel_ms / 1e3) / 1e12,
                      # the ceiling that binds the gather: one 4-byte
                      # coefficient per FMA through the 128 B/clk/SM shared-memory port
-                     "smem_gather_ceiling": smem_ceiling(fmas / B, clocks.get("sm_mhz"), kernel_ms, B),
+                     "smem_gather_ceiling": smem_ceiling(fmas / B * (2 if args.precision == 64 else 1),
+                                                         clocks.get("sm_mhz"), kernel_ms, B),
                      # the same numerator against every level: > 1 means the
                      # level is not binding (reuse above it); the SMEM frac is the binding one
                      "levels": roofline_levels(achieved, fmas / (kernel_ms / 1e3), peak, clocks.get("sm_mhz"))},

@@ -110,6 +110,19 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
 #pragma unroll
     for (int j = 0; j < RT; ++j) acc[j] = 0.0;
 
+    // x pair of the lane's rows, loaded one pair ahead (the loads are in flight
+    // during the previous pair's gather)
+    XT xa[LOC], xb[LOC];
+    auto prefetch = [&](int p) {
+#pragma unroll
+        for (int k = 0; k < LOC; ++k) {
+            const int64_t r = row0 + k * 32 + lane;
+            const bool ok = k * 32 + lane < ROWS_W && r < rows;
+            xa[k] = ok ? __ldg(X + r * n_in + 2 * p) : XT(0);
+            xb[k] = ok ? __ldg(X + r * n_in + 2 * p + 1) : XT(0);
+        }
+    };
+    prefetch(0);
     for (int p = 0; p < pairs; ++p) {
         // cells of the warp's rows for pair p (lane: rows q = k*32 + lane)
 #pragma unroll
@@ -120,8 +133,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
                 double4 w = make_double4(0.0, 0.0, 0.0, 0.0);
                 int node = 0;
                 if (r < rows) {
-                    const double x1 = static_cast<double>(X[r * n_in + 2 * p]);
-                    const double x2 = static_cast<double>(X[r * n_in + 2 * p + 1]);
+                    const double x1 = static_cast<double>(xa[k]);
+                    const double x2 = static_cast<double>(xb[k]);
                     const int i1 = cell_index<double>(x1, thr, gc.L), i2 = cell_index<double>(x2, thr, gc.L);
                     const double a = __dsub_rn(pts[i1 + 1], x1), b = __dsub_rn(x1, pts[i1]);
                     const double c = __dsub_rn(pts[i2 + 1], x2), d = __dsub_rn(x2, pts[i2]);
@@ -134,6 +147,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
                 nrec[q] = node;
             }
         }
+        if (p + 1 < pairs) prefetch(p + 1);
         __syncwarp();
         const double* sh;
         if constexpr (GSHEET) {

@@ -416,7 +416,10 @@ int forward_device_dests(const lmkan_b200_layer* L, const XT* X, const OutDests<
     if (L->exact) {  // reference precision: plain [rows][n_out] output only
         if (out.n != 1 || out.col0 != 0 || out.ld != L->n_out || im.conv)
             return fail(LMKAN_B200_EINVAL, "lmkan_forward: reference-precision layers support the plain forward only");
-        return api::forward_exact(L, X, out.base[0], rows, st);
+        if (ev_begin) cudaEventRecord(ev_begin, st);
+        const int rc = api::forward_exact(L, X, out.base[0], rows, st);
+        if (ev_end) cudaEventRecord(ev_end, st);
+        return rc;
     }
     const int cap = max_smem_optin(L->device);
     Plan pl;

@@ -1,6 +1,7 @@
-"""Copy a tools/round_bench.sh run (gpurun_out/round/) into profiles/: bench
-lines, launch lists, backward timings, ncu key metrics of the cfg2 gather
-kernel and the DRAM-traffic summary bench.py reads as roofline.traffic."""
+"""Copy a tools/round_bench.sh run (gpurun_out/round_$R/) into profiles/ as
+${R}_*: bench lines, launch lists, backward timings, ncu key metrics of the
+captured kernels and the DRAM-traffic summary bench.py reads as
+roofline.traffic (profiles/ncu_summary.json)."""
 import csv
 import json
 import os
@@ -8,7 +9,8 @@ import shutil
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "gpurun_out", "round")
+R = os.environ.get("R", "r2")
+SRC = os.path.join(ROOT, "gpurun_out", "round_" + R)
 DST = os.path.join(ROOT, "profiles")
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
 
@@ -31,22 +33,26 @@ def nbytes(m):
 
 
 def update_ncu():
-    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
             "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum",
             "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
             "launch__registers_per_thread"]
-    km_path = os.path.join(DST, "r1_ncu_key_metrics.json")
+    km_path = os.path.join(DST, f"{R}_ncu_key_metrics.json")
     km = json.load(open(km_path)) if os.path.exists(km_path) else {}
     summ_path = os.path.join(DST, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    # (capture, key-metrics entry, ncu_summary config, details csv)
-    for cap, entry, cfg, details in [("cfg2_gather", "cfg2_gather_K2", "cfg2", "r1_cfg2_gather_ncu_details.csv"),
-                                     ("cfg3_layer2_gather", "cfg3_layer2_gather_K2", "cfg3",
-                                      "r1_cfg3_layer2_gather_ncu_details.csv"),
-                                     ("cfg4_gather", "cfg4_gather_K3", "cfg4", "r1_cfg4_gather_ncu_details.csv")]:
+    # (capture, key-metrics entry, ncu_summary config or None)
+    for cap, entry, cfg in [("cfg2_gather", "cfg2_gather_K2", "cfg2"),
+                            ("cfg3_layer2_gather", "cfg3_layer2_gather_K2", "cfg3"),
+                            ("cfg3_head", "cfg3_head_narrow", None),
+                            ("cfg4_gather", "cfg4_gather_K3_pixel", "cfg4"),
+                            ("cfg1_gather", "cfg1_gather", "cfg1"),
+                            ("cfg5_gather", "cfg5_shard_gather", "cfg5")]:
         rep = os.path.join(SRC, cap + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -54,11 +60,12 @@ def update_ncu():
         km[entry] = {k: d[k] for k in keys if k in d}
         km[entry]["kernel"] = d.get("Kernel Name", {}).get("value", "")
         m = km[entry]
-        summ[cfg] = {"kernel": m["kernel"],
-                     "dram_bytes_per_launch": nbytes(m["dram__bytes_read.sum"]) + nbytes(m["dram__bytes_write.sum"]),
-                     "dram_read": nbytes(m["dram__bytes_read.sum"]), "dram_write": nbytes(m["dram__bytes_write.sum"]),
-                     "source": "profiles/r1_ncu_key_metrics.json (ncu --set full --clock-control none)"}
-        with open(os.path.join(DST, details), "w") as f:
+        if cfg:
+            summ[cfg] = {"kernel": m["kernel"],
+                         "dram_bytes_per_launch": nbytes(m["dram__bytes_read.sum"]) + nbytes(m["dram__bytes_write.sum"]),
+                         "dram_read": nbytes(m["dram__bytes_read.sum"]), "dram_write": nbytes(m["dram__bytes_write.sum"]),
+                         "source": f"profiles/{R}_ncu_key_metrics.json (ncu --set full --clock-control none)"}
+        with open(os.path.join(DST, f"{R}_{cap}_ncu_details.csv"), "w") as f:
             subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], stdout=f)
     json.dump(km, open(km_path, "w"), indent=1)
     json.dump(summ, open(summ_path, "w"), indent=1)
@@ -70,20 +77,17 @@ def main():
     update_ncu()
     if ncu_only:
         return
-    for c in (1, 2, 3, 4, 5):
-        line = last_json(os.path.join(SRC, f"bench_cfg{c}.json"))
+    for name in [f"bench_cfg{c}" for c in (1, 2, 3, 4, 5)] + ["bench_cfg2_exact", "bench_reference_cfg2"]:
+        line = last_json(os.path.join(SRC, name + ".json"))
         if line:
-            open(os.path.join(DST, f"r1_bench_cfg{c}.json"), "w").write(line + "\n")
-    line = last_json(os.path.join(SRC, "bench_reference_cfg2.json"))
-    if line:
-        open(os.path.join(DST, "r1_bench_reference_cfg2.json"), "w").write(line + "\n")
-    for c in (2, 3, 4):
+            open(os.path.join(DST, f"{R}_{name}.json"), "w").write(line + "\n")
+    for c in (1, 2, 3, 4, 5):
         p = os.path.join(SRC, f"launches_cfg{c}.csv")
         if os.path.exists(p):
-            shutil.copy(p, os.path.join(DST, f"r1_cfg{c}_launches.csv"))
+            shutil.copy(p, os.path.join(DST, f"{R}_cfg{c}_launches.csv"))
     bw = os.path.join(SRC, "bwd.jsonl")
     if os.path.exists(bw):
-        shutil.copy(bw, os.path.join(DST, "r1_bench_backward.jsonl"))
+        shutil.copy(bw, os.path.join(DST, f"{R}_bench_backward.jsonl"))
     print("profiles updated")
 
 
