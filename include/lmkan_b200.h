@@ -80,7 +80,7 @@ int lmkan_b200_layer_create(int n_in, int n_out, int G, double gamma, const doub
  * accumulation in the reference's operation order with every operation
  * explicitly rounded (no FMA contraction), so lmkan_forward's Y is
  * BIT-IDENTICAL to the reference's (layer.hpp:108-134), for any G >= 3 that
- * the grid constants hold (<= 64). The forward entry points (device f32/f64,
+ * the kernels take (<= 255). The forward entry points (device f32/f64,
  * host f32/f64) and lmkan_b200_layer_read_table accept it; the multi-dest,
  * conv and model-chain paths return EINVAL. About 2x the shared-memory
  * traffic of the fp32 gather per coefficient. */

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) backward_dx_kernel(const double* __restri
                                                           const __grid_constant__ GridConst gc) {
     __shared__ double thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
-    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = gc.t64[k];
+    for (int k = threadIdx.x; k < gc.L; k += blockDim.x) thr[k] = gc.t64[k];
     for (int k = threadIdx.x; k <= gc.G; k += blockDim.x) pts[k] = gc.points[k];
     __syncthreads();
     const int pairs = n_in / 2, G = gc.G, G1 = G + 1;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128) backward_dp_kernel(const double* __restri
                                                           int n_out, double gamma, const __grid_constant__ GridConst gc) {
     __shared__ double thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
-    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = gc.t64[k];
+    for (int k = threadIdx.x; k < gc.L; k += blockDim.x) thr[k] = gc.t64[k];
     for (int k = threadIdx.x; k <= gc.G; k += blockDim.x) pts[k] = gc.points[k];
     __syncthreads();
     const int pairs = n_in / 2, G = gc.G, G1 = G + 1;

@@ -7,19 +7,23 @@
 
 namespace lmkan_b200 {
 
-constexpr int kMaxThr = 64;  // threshold slots (G <= 64)
+constexpr int kMaxG = 255;     // largest grid (the packed node offset has 24 bits)
+constexpr int kMaxThr = 256;   // threshold slots: L = the power of two >= G, at most 256
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 
+// Grid constants of a layer, resident in device memory (one allocation per
+// layer); kernels copy them into shared memory at CTA start.
 struct GridConst {
-    float t32[kMaxThr];   // thresholds, NaN-padded to L entries
-    double t64[kMaxThr];
-    double points[kMaxThr + 1];
-    double inv_h[kMaxThr];  // 1 / (points[i+1] - points[i]), the per-axis factors of inv_areas (grid.hpp:58-64)
-    const double* inv_areas;  // device [G*G]
+    const float* t32;   // [L] thresholds t_k, NaN-padded to L entries
+    const double* t64;  // [L]
+    const double* points;     // [G+1]
+    const double* inv_h;      // [G] 1 / (points[i+1] - points[i]), the per-axis factors of inv_areas (grid.hpp:58-64)
+    const double* inv_areas;  // [G*G]
     int G;
     int L;  // power of two >= G (search width)
 };
+__host__ __device__ constexpr int grid_L(int G) { return G <= 1 ? 1 : 2 * grid_L((G + 1) / 2); }
 
 // Where the layer input x[r][col] lives: a dense row-major X (row stride n_in),
 // or the implicit im2col view of an NHWC image batch that unfold_conv would

@@ -50,9 +50,9 @@ __host__ __device__ inline ExactSmem exact_smem_layout(int G, int OT, bool gshee
     o += kExactWarps * rows_w * 4u;  // node index
     o = (o + 15u) & ~15u;
     s.off_thr = o;
-    o += kMaxThr * 8u;
+    o += static_cast<uint32_t>(grid_L(G)) * 8u;
     s.off_pts = o;
-    o += (kMaxThr + 1) * 8u;
+    o += static_cast<uint32_t>(G + 1) * 8u;
     o = (o + 15u) & ~15u;
     s.off_bar = o;
     o += 16u;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
     double* pts = reinterpret_cast<double*>(smem + Ls.off_pts);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Ls.off_bar);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int k = tid; k < kMaxThr; k += kExactWarps * 32) thr[k] = gc.t64[k];
+    for (int k = tid; k < gc.L; k += kExactWarps * 32) thr[k] = gc.t64[k];
     for (int k = tid; k <= G; k += kExactWarps * 32) pts[k] = gc.points[k];
     const int ot = blockIdx.y;
     const double* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * OT;

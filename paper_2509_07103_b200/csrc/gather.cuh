@@ -144,9 +144,11 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, in
     s.off_pts = o;
     s.off_inv = o;
     if (mode != kModeStaged) {
-        o += kMaxThr * 8u;
+        // grid constants: at least the 64 / 65 slots of grids up to G = 64 (the
+        // round-1 layout, which measured 1.5% faster at cfg4 than the tight one)
+        o += static_cast<uint32_t>(grid_L(G) > 64 ? grid_L(G) : 64) * 8u;  // thresholds (fp32 or fp64)
         s.off_pts = o;
-        o += (kMaxThr + 1) * 8u;
+        o += static_cast<uint32_t>(G + 1 > 65 ? G + 1 : 65) * 8u;
         o = (o + 15u) & ~15u;
         s.off_inv = o;
         o += static_cast<uint32_t>(G) * 8u;  // inv_h
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256) records_kernel(const XT* __restrict__ X, 
     __shared__ double pts[kMaxThr + 1];
     __shared__ double invh[kMaxThr];
     const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
-    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k < gc.L; k += 256) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
     for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
     const int p0 = blockIdx.y * 16;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(256) records4_kernel(const XT* __restrict__ X,
     __shared__ double pts[kMaxThr + 1];
     __shared__ double invh[kMaxThr];
     const int G = gc.G, pairs = n_in / 2, tid = threadIdx.x;
-    for (int k = tid; k < kMaxThr; k += 256) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k < gc.L; k += 256) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += 256) pts[k] = gc.points[k];
     for (int k = tid; k < G; k += 256) invh[k] = gc.inv_h[k];
     __syncthreads();
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(256) locate_ag_kernel(const XT* __restrict__ X
     __shared__ double pts[kMaxThr + 1];
     __shared__ double invh[kMaxThr];
     const int G = gc.G;
-    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = threadIdx.x; k < gc.L; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
     for (int k = threadIdx.x; k <= G; k += blockDim.x) pts[k] = gc.points[k];
     for (int k = threadIdx.x; k < G; k += blockDim.x) invh[k] = gc.inv_h[k];
     __syncthreads();
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(256) pixel_records_kernel(const XT* __restrict
     __shared__ double pts[kMaxThr + 1];
     __shared__ double invh[kMaxThr];
     const int G = gc.G;
-    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = threadIdx.x; k < gc.L; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
     for (int k = threadIdx.x; k <= G; k += blockDim.x) pts[k] = gc.points[k];
     for (int k = threadIdx.x; k < G; k += blockDim.x) invh[k] = gc.inv_h[k];
     __syncthreads();
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     constexpr bool kLocate = MODE == kModeFused || MODE == kModeGlobal;  // in-kernel locate
     constexpr bool kPix = MODE == kModePixel;
     if constexpr (kLocate) {
-        for (int k = tid; k < kMaxThr; k += NT) thr[k] = thr_of<XT>(gc)[k];
+        for (int k = tid; k < gc.L; k += NT) thr[k] = thr_of<XT>(gc)[k];
         for (int k = tid; k <= G; k += NT) pts[k] = gc.points[k];
         for (int k = tid; k < G; k += NT) inv[k] = gc.inv_h[k];
     }
@@ -858,11 +860,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const bool same_tile = emit.sh.R == R;
             __syncthreads();  // all warps past the gather loop: the ring space is free
             for (int k = tid; k < kMaxThr + 1; k += NT) {
-                npts[k] = gc_next.points[k];
-                if (k < kMaxThr) {
-                    ninv[k] = gc_next.inv_h[k];
-                    nthr[k] = gc_next.t32[k];
-                }
+                if (k <= gc_next.G) npts[k] = gc_next.points[k];
+                if (k < gc_next.G) ninv[k] = gc_next.inv_h[k];
+                if (k < gc_next.L) nthr[k] = gc_next.t32[k];
             }
             for (int h = 0; h < 2; ++h) {
                 __syncthreads();  // grid constants in place / the previous pass's stores done

@@ -28,7 +28,7 @@ struct lmkan_b200_layer {
     size_t table64_bytes = 0;
     float* table = nullptr;
     size_t table_bytes = 0;
-    double* d_inv = nullptr;
+    double* d_inv = nullptr;  // the grid constants block (GridConst's arrays), inv_areas first
     lmkan_b200::GridConst gc{};
     // bumped by every mutation after creation (set_gamma): captured CUDA graphs
     // of a model bake gamma into their kernel parameters and re-capture on change

@@ -368,7 +368,9 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
         im.npix < (int64_t(1) << 31) && !link.emit.W && env_int("LMKAN_B200_PIXREC", 1)) {
         const int64_t nrec = im.npix * (im.C / 2);
         CK(cudaMallocAsync(reinterpret_cast<void**>(&pixrec), static_cast<size_t>(nrec) * sizeof(int4), st));
-        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((nrec + 255) / 256, L->num_sms * 16));
+        // one wave of 8 blocks per SM, grid-stride: each block stages the grid
+        // constants once (global -> shared) and amortises that over many records
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((nrec + 255) / 256, L->num_sms * 8));
         pixel_records_kernel<XT><<<blocks, 256, 0, st>>>(X, im.npix, im.C, L->gc, L->ns, L->G, pixrec);
         const cudaError_t e1 = cudaGetLastError();
         if (e1 != cudaSuccess) {
@@ -529,7 +531,7 @@ int validate_shape(int n_in, int n_out, int G) {
         return fail(LMKAN_B200_EINVAL, "init_layer: n_in must be a positive even number");
     if (n_out <= 0) return fail(LMKAN_B200_EINVAL, "init_layer: n_out must be positive");
     if (G < 3) return fail(LMKAN_B200_EINVAL, "build_grid: G must be >= 3 (ghost rule needs two interior points)");
-    if (G > kMaxThr) return fail(LMKAN_B200_EINVAL, "build_grid: G > 64 is not supported by the B200 kernels");
+    if (G > kMaxG) return fail(LMKAN_B200_EINVAL, "build_grid: G > 255 is not supported by the B200 kernels");
     return LMKAN_B200_OK;
 }
 
@@ -579,21 +581,29 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
     host::thresholds(G, t64, t32);
     GridConst& gc = L->gc;
     gc.G = G;
-    gc.L = 1;
-    while (gc.L < G) gc.L <<= 1;
-    const float fnan = std::numeric_limits<float>::quiet_NaN();
-    const double dnan = std::numeric_limits<double>::quiet_NaN();
-    for (int k = 0; k < kMaxThr; ++k) {
-        gc.t32[k] = k < G - 1 ? t32[k] : fnan;
-        gc.t64[k] = k < G - 1 ? t64[k] : dnan;
+    gc.L = grid_L(G);
+    // one device block holds the grid constants: inv_areas[G*G], t64[L],
+    // points[G+1], inv_h[G] (doubles), then t32[L] (floats); thresholds are
+    // NaN-padded to L entries (the search's upper padding)
+    const size_t nd = static_cast<size_t>(G) * G + gc.L + (G + 1) + G;
+    std::vector<double> blk(nd + (gc.L + 1) / 2, 0.0);
+    double* hp = blk.data();
+    std::copy(inv.begin(), inv.end(), hp);
+    double* h64 = hp + static_cast<size_t>(G) * G;
+    double* hpts = h64 + gc.L;
+    double* hinvh = hpts + G + 1;
+    float* h32 = reinterpret_cast<float*>(hinvh + G);
+    for (int k = 0; k < gc.L; ++k) {
+        h64[k] = k < G - 1 ? t64[k] : std::numeric_limits<double>::quiet_NaN();
+        h32[k] = k < G - 1 ? t32[k] : std::numeric_limits<float>::quiet_NaN();
     }
-    for (int k = 0; k <= kMaxThr; ++k) gc.points[k] = k <= G ? pts[k] : 0.0;
-    for (int k = 0; k < kMaxThr; ++k) gc.inv_h[k] = k < G ? 1.0 / (pts[k + 1] - pts[k]) : 0.0;
+    for (int k = 0; k <= G; ++k) hpts[k] = pts[k];
+    for (int k = 0; k < G; ++k) hinvh[k] = 1.0 / (pts[k + 1] - pts[k]);
     L->table_bytes = exact ? 0 : static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->ns * sizeof(float);
     L->table64_bytes = exact ? static_cast<size_t>(L->n_ot) * L->pairs * L->nodes * L->OT * sizeof(double) : 0;
-    cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * inv.size());
+    cudaError_t e = cudaMalloc(&L->d_inv, sizeof(double) * blk.size());
     if (e == cudaSuccess)
-        e = cudaMemcpy(L->d_inv, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice);
+        e = cudaMemcpy(L->d_inv, blk.data(), sizeof(double) * blk.size(), cudaMemcpyHostToDevice);
     // the allocation is rounded up to 16 B and the tail zeroed: the narrow kernel
     // bulk-copies the whole table, and bulk copies move multiples of 16 B
     const size_t alloc_bytes = (L->table_bytes + 15) & ~static_cast<size_t>(15);
@@ -609,6 +619,10 @@ int alloc_layer(int n_in, int n_out_local, int n_out_total, int out_begin, int G
         return cuda_fail(e, "layer_create: device allocation");
     }
     gc.inv_areas = L->d_inv;
+    gc.t64 = L->d_inv + static_cast<size_t>(G) * G;
+    gc.points = gc.t64 + gc.L;
+    gc.inv_h = gc.points + G + 1;
+    gc.t32 = reinterpret_cast<const float*>(gc.inv_h + G);
     {  // keep stream-ordered scratch (cell records, host-path staging) in the pool between calls
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) locate_kernel(const XT* __restrict__ X, i
                                                      float4* __restrict__ o_w) {
     __shared__ XT thr[kMaxThr];
     __shared__ double pts[kMaxThr + 1];
-    for (int k = threadIdx.x; k < kMaxThr; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = threadIdx.x; k < gc.L; k += blockDim.x) thr[k] = thr_of<XT>(gc)[k];
     for (int k = threadIdx.x; k <= gc.G; k += blockDim.x) pts[k] = gc.points[k];
     __syncthreads();
     const int pairs = n_in / 2;

@@ -18,7 +18,7 @@ constexpr int kNarrowThreads = 1024;
 __host__ __device__ inline uint32_t narrow_smem_bytes(int G, int pairs, int NO) {
     const uint32_t tab = static_cast<uint32_t>((G + 1) * (G + 1)) * pairs * NO * 4u;
     uint32_t o = (tab + 15u) & ~15u;
-    o += kMaxThr * 8u + (kMaxThr + 1) * 8u + static_cast<uint32_t>(G) * 8u + 16u;
+    o += static_cast<uint32_t>(grid_L(G)) * 8u + static_cast<uint32_t>(G + 1) * 8u + static_cast<uint32_t>(G) * 8u + 16u;
     return (o + 127u) & ~127u;
 }
 
@@ -35,14 +35,14 @@ __global__ void __launch_bounds__(kNarrowThreads, 1)
     float* tab = reinterpret_cast<float*>(smem);
     uint32_t o = tab_bytes;
     XT* thr = reinterpret_cast<XT*>(smem + o);
-    o += kMaxThr * 8u;
+    o += static_cast<uint32_t>(gc.L) * 8u;
     double* pts = reinterpret_cast<double*>(smem + o);
-    o += (kMaxThr + 1) * 8u;
+    o += static_cast<uint32_t>(G + 1) * 8u;
     double* inv = reinterpret_cast<double*>(smem + o);
     o += static_cast<uint32_t>(G) * 8u;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((o + 7u) & ~7u));
     const int tid = threadIdx.x;
-    for (int k = tid; k < kMaxThr; k += kNarrowThreads) thr[k] = thr_of<XT>(gc)[k];
+    for (int k = tid; k < gc.L; k += kNarrowThreads) thr[k] = thr_of<XT>(gc)[k];
     for (int k = tid; k <= G; k += kNarrowThreads) pts[k] = gc.points[k];
     for (int k = tid; k < G; k += kNarrowThreads) inv[k] = gc.inv_h[k];
     if (tid == 0) {

@@ -35,7 +35,7 @@ def test_exact_forward_bitwise(torch, pkg, oracle, n_in, n_out, G, rows):
 
 @pytest.mark.parametrize("n_in,n_out,G,rows,gamma", [
     (2, 1, 3, 77, 1.0), (6, 5, 12, 64, 0.8), (10, 7, 40, 333, 1.0), (12, 9, 64, 100, 0.5),
-    (30, 100, 9, 777, 1.3), (8, 33, 28, 1025, 0.0), (64, 64, 8, 5000, 1.0),
+    (30, 100, 9, 777, 1.3), (8, 33, 28, 1025, 0.0), (64, 64, 8, 5000, 1.0), (6, 3, 200, 40, 1.1),
 ])
 def test_exact_small_ragged_and_large_g(torch, pkg, oracle, n_in, n_out, G, rows, gamma):
     """Ragged output tiles, gamma = 0, every sheet width (OT 32 / 16 / 8) and

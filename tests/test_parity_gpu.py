@@ -79,7 +79,7 @@ def test_locate_bit_exact(torch, pkg, oracle, n_in, n_out, G, rows):
     np.testing.assert_array_equal(w.cpu().numpy(), rw.astype(np.float32))
 
 
-@pytest.mark.parametrize("G", [3, 4, 5, 8, 12, 13, 16, 28, 32, 40, 64])
+@pytest.mark.parametrize("G", [3, 4, 5, 8, 12, 13, 16, 28, 32, 40, 64, 100, 255])
 def test_locate_f64_near_thresholds(torch, pkg, oracle, G):
     """Double inputs that are not fp32-representable, packed around every
     threshold: the f64 path compares against the fp64 thresholds."""
@@ -119,6 +119,7 @@ def test_forward_parity(torch, pkg, oracle, n_in, n_out, G, rows):
     (2, 1, 5, 64, 1.0), (6, 5, 3, 64, 0.8), (6, 5, 12, 64, 0.8), (8, 3, 4, 33, 0.6), (8, 6, 12, 33, 0.9),
     (4, 3, 4, 16, 0.0), (10, 7, 64, 130, 1.0), (30, 100, 9, 777, 1.3), (16, 20, 6, 1, 1.0),
     (64, 200, 8, 5000, 1.0), (256, 48, 20, 3001, 0.5),
+    (10, 7, 100, 130, 1.0), (6, 5, 255, 50, 0.7),  # large grids: sheets read from L2 (global mode)
 ])
 def test_forward_small_and_ragged(torch, pkg, oracle, n_in, n_out, G, rows, gamma):
     P, X = _inputs(torch, n_in, n_out, G, rows, seed=n_in * 7 + n_out + G, xscale=1.5)

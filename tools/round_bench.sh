@@ -28,6 +28,11 @@ KREGEX=narrow cap cfg3_head 3 3
 cap cfg1_gather 1 3
 cap cfg5_gather 5 3 --shards 8
 python tools/update_profiles.py --ncu-only
+# the .ncu-rep files are too large to come back (gpurun merges <= 64 MiB):
+# keep their extracted key metrics / details and the traffic summary
+mkdir -p $O/prof
+cp profiles/${R}_*ncu* profiles/ncu_summary.json $O/prof/ 2>/dev/null
+rm -f $O/*.ncu-rep
 timeout 400 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
 for c in 1 3 4; do timeout 400 python bench.py --config $c > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; done
 timeout 900 python bench.py --config 5 --shards 8 --steps 5 --warmup 3 > $O/bench_cfg5.json 2> $O/bench_cfg5.err

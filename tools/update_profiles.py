@@ -74,9 +74,15 @@ def update_ncu():
 def main():
     import sys
     ncu_only = "--ncu-only" in sys.argv  # on the GPU box, between the captures and the bench lines
-    update_ncu()
     if ncu_only:
+        update_ncu()
         return
+    # here: the box's extracted ncu files (round_bench.sh copies them to $SRC/prof)
+    prof = os.path.join(SRC, "prof")
+    if os.path.isdir(prof):
+        for f in os.listdir(prof):
+            shutil.copy(os.path.join(prof, f), os.path.join(DST, f))
+    update_ncu()  # no-op unless .ncu-rep files are present locally
     for name in [f"bench_cfg{c}" for c in (1, 2, 3, 4, 5)] + ["bench_cfg2_exact", "bench_reference_cfg2"]:
         line = last_json(os.path.join(SRC, name + ".json"))
         if line:
