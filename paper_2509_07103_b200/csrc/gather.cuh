@@ -511,9 +511,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     __syncthreads();
 
-    auto issue = [&](int u) {  // one thread: slab (+ the pair's records when staged) of unit u
-        const int p = u / S, s = u - p * S;
-        const int slot = u % nbuf;
+    // one thread: slab (+ the pair's records when staged) of unit u into ring
+    // slot `slot` (= u % nbuf; passed in, the loop tracks it without divisions)
+    auto issue = [&](int u, int slot) {
+        const int p = SLAB ? u / S : u, s = SLAB ? u - p * S : 0;
         const uint32_t bytes = static_cast<uint32_t>(slab_node_rows(G, H, s)) * (G + 1) * NS * 4u;
         const bool with_rec = MODE == kModeStaged && s == 0;
         mbar_arrive_expect_tx(&full[slot], bytes + (with_rec ? recw_copy + L.reco_bytes : 0u));
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         if constexpr (MODE == kModeStaged) {
             if (with_rec) {
-                const int rs = p % L.nrec;
+                const int rs = SLAB ? p % L.nrec : slot;  // unslabbed: nrec == nbuf and p == u
                 bulk_g2s(reinterpret_cast<char*>(rec_w) + rs * L.recw_bytes,
                          recW + static_cast<size_t>(p) * rows_pad + row0, recw_copy, &full[slot], policy_rec);
                 if (L.reco_bytes)
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if constexpr (kSmemSheet) {
         if (tid == 0) {
             const int pre = nbuf < units ? nbuf : units;
-            for (int u = 0; u < pre; ++u) issue(u);
+            for (int u = 0; u < pre; ++u) issue(u, u);
         }
     }
 
@@ -714,6 +715,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if constexpr (GOFF) load_offs(offs_src(0), offs_next, true);
     const float2* rw = rec_w;
     int p = 0, s = 0;
+    int slot = 0;         // u % nbuf
+    uint32_t phase = 0;   // (u / nbuf) & 1: the "landed" mbarrier phase of unit u
     // units in pair blocks: the loop body is the same for every block, the
     // running-sum fold sits between blocks (one block when pair_block == 0)
     const int blk_units = (pair_block > 0 ? pair_block : pairs) * S;
@@ -722,14 +725,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
         for (int u = u0; u < u1; ++u) {
             const float* sh;
             if constexpr (kSmemSheet) {
-                const int slot = u % nbuf;
-                mbar_wait(&full[slot], static_cast<uint32_t>((u / nbuf) & 1));
+                mbar_wait(&full[slot], phase);
                 sh = sheets + static_cast<size_t>(slot) * (L.sheet_bytes / 4) + lane_base;
             } else {
                 sh = tsrc + static_cast<size_t>(p) * sheet_floats + lane_base;
             }
             if (!SLAB || s == 0) {  // pair's records: weights stay in smem, offsets in registers (kept across slabs)
-                const int rs = MODE == kModeStaged ? p % L.nrec : 0;
+                const int rs = MODE == kModeStaged ? (SLAB ? p % L.nrec : slot) : 0;
                 rw = rec_w + rs * (L.recw_bytes / 8) + warp * Sh::ROWS_W + sub;
                 if constexpr (GOFF) {
 #pragma unroll
@@ -803,7 +805,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
             __syncwarp();  // this warp is done with slot u % nbuf (and, at s == S-1, with pair p's records)
             if constexpr (kSmemSheet) {
                 if (lane == 0) {
-                    const int slot = u % nbuf;
                     // acq_rel increment: releases this warp's reads of the slot (ordered
                     // before it by __syncwarp) and, for the last warp, acquires everyone
                     // else's, so all reads happen before the async-proxy overwrite below
@@ -811,9 +812,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
                         cnt[slot] = 0;
                         if (u + nbuf < units) {
                             fence_proxy_async();
-                            issue(u + nbuf);
+                            issue(u + nbuf, slot);
                         }
                     }
+                }
+                if (++slot == nbuf) {  // ring position of the next unit
+                    slot = 0;
+                    phase ^= 1u;
                 }
             }
             if (++s == S) {
