@@ -55,3 +55,28 @@ bufs = [torch.zeros((300, 48), device="cuda") for _ in range(3)]
 sl.forward_dests(torch.randn((300, 64), device="cuda"), [b.data_ptr() for b in bufs], 48, 16)
 torch.cuda.synchronize()
 print("dests", float(bufs[2].abs().sum()))
+# round 2: half-swapped plain OT = 16 sheets (staged + fused), pair-block
+# summation, narrow pair blocks, pixel-record conv, reference precision (every
+# sheet width and the L2-sheet variant), production-record dumps, large grids,
+# pageable host staging
+run({}, 64, 16, 28, 2000)                               # plain OT 16, half swap, staged
+run({"LMKAN_B200_MODE": "fused"}, 64, 16, 28, 2000)     # half swap, in-kernel locate
+run({"LMKAN_B200_PAIR_BLOCK": "4"}, 40, 24, 8, 900)     # pair blocks (fold into Y)
+run({"LMKAN_B200_PAIR_BLOCK": "4"}, 46, 3, 8, 700)      # narrow kernel pair blocks
+run({}, 10, 7, 100, 300)                                # G = 100: global-sheet mode
+lay = pkg.Layer.random(9 * 32, 32, 16, seed=7)
+print("conv pixel", float(lay.conv_forward(torch.randn((2, 12, 12, 32), device="cuda"), 3, 1).abs().sum()))
+for n_in, n_out, G in [(64, 64, 8), (30, 40, 28), (12, 9, 40), (6, 3, 200)]:
+    Pe = np.random.default_rng(G).standard_normal((G + 1, G + 1, n_in // 2, n_out))
+    le = pkg.Layer.from_host(n_in, n_out, G, Pe, 0.9, precision=64)
+    Ye = le.forward(torch.randn((700, n_in), device="cuda", dtype=torch.float64))
+    torch.cuda.synchronize()
+    print("exact", G, float(Ye.abs().sum()))
+lr = pkg.Layer.random(64, 16, 28, seed=8)
+Xr = torch.randn((600, 64), device="cuda")
+for v in ("k1", "k1_smem", "in_kernel"):
+    i1, i2, ag = lr.records(Xr, v)
+torch.cuda.synchronize()
+print("records", int(i1.sum()), int(i2.sum()))
+lh = pkg.Layer.random(96, 80, 12, seed=9)
+print("host staging", float(np.abs(lh.forward_host(np.random.default_rng(1).standard_normal((20000, 96)))).sum()))
