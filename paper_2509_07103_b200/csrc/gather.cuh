@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // conflict-free loads of plain (not duplicated) OT = 16 sheets by bank-half
     // swapped records (locate_ag's hsub; the gather loop un-swaps)
     constexpr bool kHalfSwap = OT == 16 && !DUP && V == 1 && kSmemSheet && !SLAB;
+
     constexpr bool kLocate = MODE == kModeFused || MODE == kModeGlobal;  // in-kernel locate
     constexpr bool kPix = MODE == kModePixel;
     if constexpr (kLocate) {

@@ -163,8 +163,8 @@ __device__ __forceinline__ float4 weights_ag(float2 ag) {
 // latency-bound gathers it measured slower (config 3 chain 5.86 -> 6.08 ms,
 // config 2 +0.5%), so they keep the scalar form.
 template <bool PACKED = false>
-__device__ __forceinline__ void fma_corners(float4& acc, const float4 w, const float4 p00, const float4 p10,
-                                            const float4 p01, const float4 p11) {
+__device__ __forceinline__ float4 corner_term(const float4 w, const float4 p00, const float4 p10, const float4 p01,
+                                              const float4 p11) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     if constexpr (PACKED) {
         const float2 w0 = make_float2(w.x, w.x), w1 = make_float2(w.y, w.y), w2 = make_float2(w.z, w.z),
@@ -177,15 +177,33 @@ __device__ __forceinline__ void fma_corners(float4& acc, const float4 w, const f
                                      __ffma2_rn(w2, make_float2(p01.z, p01.w),
                                                 __ffma2_rn(w1, make_float2(p10.z, p10.w),
                                                            __fmul2_rn(w0, make_float2(p00.z, p00.w)))));
-        const float2 a = __fadd2_rn(make_float2(acc.x, acc.y), lo), b = __fadd2_rn(make_float2(acc.z, acc.w), hi);
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+#endif
+    return make_float4(fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x))),
+                       fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y))),
+                       fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z))),
+                       fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w))));
+}
+template <bool PACKED = false>
+__device__ __forceinline__ void acc_add(float4& acc, const float4 t) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    if constexpr (PACKED) {
+        const float2 a = __fadd2_rn(make_float2(acc.x, acc.y), make_float2(t.x, t.y));
+        const float2 b = __fadd2_rn(make_float2(acc.z, acc.w), make_float2(t.z, t.w));
         acc = make_float4(a.x, a.y, b.x, b.y);
         return;
     }
 #endif
-    acc.x += fmaf(w.w, p11.x, fmaf(w.z, p01.x, fmaf(w.y, p10.x, w.x * p00.x)));
-    acc.y += fmaf(w.w, p11.y, fmaf(w.z, p01.y, fmaf(w.y, p10.y, w.x * p00.y)));
-    acc.z += fmaf(w.w, p11.z, fmaf(w.z, p01.z, fmaf(w.y, p10.z, w.x * p00.z)));
-    acc.w += fmaf(w.w, p11.w, fmaf(w.z, p01.w, fmaf(w.y, p10.w, w.x * p00.w)));
+    acc.x += t.x;
+    acc.y += t.y;
+    acc.z += t.z;
+    acc.w += t.w;
+}
+template <bool PACKED = false>
+__device__ __forceinline__ void fma_corners(float4& acc, const float4 w, const float4 p00, const float4 p10,
+                                            const float4 p01, const float4 p11) {
+    acc_add<PACKED>(acc, corner_term<PACKED>(w, p00, p10, p01, p11));
 }
 
 }  // namespace lmkan_b200
