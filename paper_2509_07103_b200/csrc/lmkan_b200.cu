@@ -157,8 +157,10 @@ int choose_pair_block(int pairs) {
 // Within a mode: prefer double buffering with the fewest slabs, then the
 // largest row tile that still fills the GPU with one wave of CTAs.
 bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out, int force_mode_arg = -1) {
-    // ring depth: up to 4 (deeper rings measured no faster at cfg1-4; LMKAN_B200_MAX_NBUF overrides)
-    const int max_nbuf = std::max(2, std::min(16, env_int("LMKAN_B200_MAX_NBUF", 4)));
+    // ring depth: up to 8, as deep as shared memory allows (cfg4's 37 KB DUP
+    // sheets: 5 slots, 0.2353 -> 0.2313 ms vs 4; cfg1/2/3/5 unchanged: their
+    // sheets fit 2-4 slots); LMKAN_B200_MAX_NBUF overrides
+    const int max_nbuf = std::max(2, std::min(16, env_int("LMKAN_B200_MAX_NBUF", 8)));
     const int force_rt = env_int("LMKAN_B200_RT", 0), force_nbuf = env_int("LMKAN_B200_NBUF", 0),
               force_s = env_int("LMKAN_B200_SLABS", 0);
     if (L->narrow) {
