@@ -236,9 +236,11 @@ int lmkan_b200_records_f64(const lmkan_b200_layer* layer, const double* X_dev, i
 int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, int* rows_per_thread,
                     int* nbuf, int* rows_per_cta, int* launches, int* mode, int* slabs, int* warps_per_cta);
 /* Float4 runs of outputs each gather lane covers at output tile `out_tile`
- * (4 at 64, else 1): rows_per_thread x this = the per-thread register tile in
+ * (4 at 64, 2 at 32, else 1): rows_per_thread x this = the per-thread register tile in
  * float4s, the quantity LMKAN_B200_RT / the small-batch path are sized by. */
 int lmkan_b200_lane_vectors(int out_tile);
+/* The same for a layer (duplicated-node OT = 16 tables use 2 runs of 32 B). */
+int lmkan_b200_layer_lane_vectors(const lmkan_b200_layer* layer);
 
 /* ---- training path ----
  *

@@ -356,7 +356,10 @@ class Layer:
                       "warps_per_cta"],
                      [x.value for x in v]))
         d["mode"] = {0: "fused", 1: "staged", 2: "global", 3: "narrow", 4: "exact"}[d["mode"]]
-        d["lane_vectors"] = int(lib.lmkan_b200_lane_vectors(d["out_tile"]))
+        if hasattr(lib, "lmkan_b200_layer_lane_vectors"):
+            d["lane_vectors"] = int(lib.lmkan_b200_layer_lane_vectors(self._h))
+        else:  # an older build under A/B (LMKAN_B200_LIB)
+            d["lane_vectors"] = int(lib.lmkan_b200_lane_vectors(d["out_tile"]))
         return d
 
     def close(self) -> None:

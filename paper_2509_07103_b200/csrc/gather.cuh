@@ -32,14 +32,20 @@ enum : int {
 #ifndef LMKAN_B200_VEC32
 #define LMKAN_B200_VEC32 2
 #endif
-__host__ __device__ constexpr int lane_vectors(int OT) {
-    return OT >= 64 ? LMKAN_B200_VEC64 : (OT == 32 ? LMKAN_B200_VEC32 : 1);
+// OT = 16 with a duplicated-node table (NS = 2 OT): two 32-B runs per lane,
+// 16 rows per instruction (see fwd_fused_kernel's bank mapping); plain OT = 16
+// keeps one run (its bank-half swap needs whole 64-B runs).
+#ifndef LMKAN_B200_VEC16D
+#define LMKAN_B200_VEC16D 2
+#endif
+__host__ __device__ constexpr int lane_vectors(int OT, int NS = 0) {
+    return OT >= 64 ? LMKAN_B200_VEC64 : (OT == 32 ? LMKAN_B200_VEC32 : (NS == 2 * OT ? LMKAN_B200_VEC16D : 1));
 }
 
 // Row <-> thread mapping shared by K1 (which writes records in K2's order) and K2.
-template <int OT, int RT, int NW = kWarps>
+template <int OT, int RT, int NW = kWarps, bool DUP = false>
 struct FusedShape {
-    static constexpr int V = lane_vectors(OT);       // float4 runs per lane
+    static constexpr int V = lane_vectors(OT, DUP ? 2 * OT : 0);  // float4 runs per lane
     static constexpr int LPR = OT / (4 * V);         // lanes covering one row's OT outputs
     static constexpr int RPW = 32 / LPR;             // rows per warp per gather instruction
     static constexpr int ROWS_W = RPW * RT;          // rows owned by one warp
@@ -61,7 +67,7 @@ __host__ __device__ inline ShapeRT shape_rt(int OT, int RT, int NW = kWarps, int
     s.NS = NS > 0 ? NS : OT;
     s.RT = RT;
     s.NW = NW;
-    s.LPR = OT / (4 * lane_vectors(OT));
+    s.LPR = OT / (4 * lane_vectors(OT, s.NS));
     s.RPW = 32 / s.LPR;
     s.ROWS_W = s.RPW * RT;
     s.R = NW * s.ROWS_W;
@@ -117,7 +123,7 @@ struct FusedSmem {
 };
 __host__ __device__ inline FusedSmem fused_smem_layout(int G, int OT, int RT, int nbuf, int mode, int S = 1,
                                                        int NW = kWarps, int NS = 0, int goff = 0) {
-    const ShapeRT sh = shape_rt(OT, RT, NW);
+    const ShapeRT sh = shape_rt(OT, RT, NW, NS);
     const int H = (G + S - 1) / S;
     const int nb = nbuf > 0 ? nbuf : 1;
     FusedSmem s;
@@ -441,13 +447,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
                      const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im, const EmitRecords emit,
                      const __grid_constant__ GridConst gc_next, int Rt_arg, int pair_block) {
-    using Sh = FusedShape<OT, RT, NW>;
+    using Sh = FusedShape<OT, RT, NW, DUP>;
     constexpr int R = Sh::R;
     const int Rt = TAIL ? Rt_arg : R;  // full-tile kernels keep the row tile a compile-time constant
     constexpr int NT = NW * 32;
     constexpr bool kSmemSheet = MODE != kModeGlobal;
     constexpr int NS = DUP ? 2 * OT : OT;  // node stride in the table / sheets (floats)
-    static_assert(!DUP || (!SLAB && MODE != kModeGlobal && lane_vectors(OT) == 1), "DUP: unslabbed smem sheets");
+    static_assert(!DUP || (!SLAB && MODE != kModeGlobal), "DUP: unslabbed smem sheets");
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G;
     const int nodes = (G + 1) * (G + 1);
@@ -471,8 +477,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // Float offset of the lane's v-th run. Runs of 64 B (OT / V = 16) sit on one
     // bank half each (nodes are 128-B aligned); odd lane groups take the runs in
     // the order 1 0 3 2, so every instruction puts half its rows on each bank
-    // half: 8 rows x 64 B in 4 wavefronts, no conflicts.
-    const int vflip = (V >= 2 && VSTEP == 16) ? (sub & 1) : 0;
+    // half: 8 rows x 64 B in 4 wavefronts, no conflicts. DUP at V = 2: a node's
+    // 128-B line holds its two copies; lane group `sub` reads copy sub & 1 and
+    // its two 32-B runs in the order given by (sub >> 1) & 1, so each 8-bank
+    // quarter of an instruction gets 4 of its 16 rows: 4 wavefronts, no conflicts.
+    const int vflip = V >= 2 ? (VSTEP == 16 ? (sub & 1) : ((sub >> 1) & 1)) : 0;
     auto vofs = [&](int v) { return (v ^ vflip) * VSTEP; };
     const int lane_base = 4 * c4 + (DUP ? (sub & 1) * OT : 0);  // DUP: odd lane groups read the second copy
     const int64_t tile = blockIdx.x;
@@ -647,7 +656,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bx_));
         asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(by_));
         const int w_ = static_cast<int>(t_ >> 5), sb = static_cast<int>(t_ & 31) / Sh::LPR;
-        const int vf = (V >= 2 && VSTEP == 16) ? (sb & 1) : 0;
+        const int vf = V >= 2 ? (VSTEP == 16 ? (sb & 1) : ((sb >> 1) & 1)) : 0;
         const int cl = static_cast<int>(by_) * OT + 4 * (static_cast<int>(t_ & 31) % Sh::LPR);
         const int64_t ld = out.ld;
         XT* const base = out.base[0] + out.col0;

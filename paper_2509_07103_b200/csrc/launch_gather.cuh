@@ -34,7 +34,7 @@ cudaError_t launch_fused_rt(const lmkan_b200_layer* L, const Plan& pl, const XT*
                             const float2* recW, const int* recO, const InputMap& im, const EmitRecords& emit,
                            const GridConst* gc_next, cudaStream_t st) {
     // rows per thread: the planner's {16, 8, 4} float4 accumulators per thread / V
-    constexpr int V = lane_vectors(OT);
+    constexpr int V = lane_vectors(OT, DUP ? 2 * OT : 0);
     constexpr int RT0 = 16 / V, RT1 = 8 / V, RT2 = 4 / V;
     if constexpr (MODE == kModeStaged && !SLAB && !DUP) {  // offsets from global: the tallest tile only (planner)
         if (pl.goff) {

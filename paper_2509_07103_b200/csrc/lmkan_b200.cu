@@ -129,7 +129,7 @@ int choose_out_tile(int n_out, int G, int smem_cap) {
 // G = 16: 37 KB; not G = 28 / 32: 108 / 139 KB). LMKAN_B200_DUP16=0 disables.
 bool choose_dup(int OT, int G, int smem_cap) {
     if (OT != 16 || !env_int("LMKAN_B200_DUP16", 1)) return false;
-    const int RT = kRTChoices[0] / lane_vectors(OT);
+    const int RT = kRTChoices[0] / lane_vectors(OT, 2 * OT);
     return static_cast<int>(fused_smem_layout(G, OT, RT, 2, kModeFused, 1, kWarps, 2 * OT).total) <= smem_cap &&
            static_cast<int>(fused_smem_layout(G, OT, RT, 2, kModeStaged, 1, kWarps, 2 * OT).total) <= smem_cap;
 }
@@ -178,8 +178,9 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
     // staged when >= 3 output tiles re-read the cells, or when the batch is too
     // small to give every SM a 16-warp CTA (the per-pair locate then sits on the
     // critical path of the few rows each CTA owns; measured 32 vs 47 us at cfg1)
-    const int rt_small = kRTChoices[2] / lane_vectors(L->OT);
-    const bool small = ((rows + shape_rt(L->OT, rt_small).R - 1) / shape_rt(L->OT, rt_small).R) * L->n_ot < L->num_sms;
+    const int rt_small = kRTChoices[2] / lane_vectors(L->OT, L->ns);
+    const int r_small = shape_rt(L->OT, rt_small, kWarps, L->ns).R;
+    const bool small = ((rows + r_small - 1) / r_small) * L->n_ot < L->num_sms;
     const int NSt = L->ns;  // node stride of the table (2 OT for duplicated-node tables)
     const int pref = (L->n_ot >= 3 || small) ? kModeStaged : kModeFused;
     const int modes[3] = {pref, pref == kModeStaged ? kModeFused : kModeStaged, kModeGlobal};
@@ -193,7 +194,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                 if (force_s && S != force_s) continue;
                 if (S > 1 && (min_buf == 1 || L->dup)) continue;
                 for (int A : kRTChoices) {
-                    const int RT = A / lane_vectors(L->OT);
+                    const int RT = A / lane_vectors(L->OT, L->ns);
                     if (force_rt && RT != force_rt) continue;
                     if (mode == kModeGlobal && A != kRTChoices[2]) continue;  // the global-sheet kernel is built for RT2 only
                     // warps per CTA: 16, or for batches too small to give every SM a
@@ -1168,6 +1169,10 @@ int lmkan_b200_records_f64(const lmkan_b200_layer* L, const double* X, int32_t* 
 }
 
 int lmkan_b200_lane_vectors(int out_tile) { return lane_vectors(out_tile); }
+int lmkan_b200_layer_lane_vectors(const lmkan_b200_layer* L) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "lane_vectors: null layer"), 0;
+    return L->narrow || L->exact ? 1 : lane_vectors(L->OT, L->ns);
+}
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,
                     int* rows_per_cta_out, int* launches, int* mode, int* slabs, int* warps_per_cta) {

@@ -493,9 +493,10 @@ def test_duplicated_node_tables_bitwise(torch, pkg, oracle, monkeypatch, n_in, n
     np.testing.assert_array_equal(layers["1"].read_table(), P.astype(np.float64))
     np.testing.assert_array_equal(layers["rand1"].read_table(), layers["rand0"].read_table())
     base = layers["0"].forward(Xd)
+    lv = layers["1"].plan(rows)["lane_vectors"]  # 2: two 32-B runs per lane on duplicated-node tables
     for mode in ("fused", "staged"):
         monkeypatch.setenv("LMKAN_B200_MODE", mode)
-        for rt in ("16", "8", "4"):
+        for rt in (str(16 // lv), str(8 // lv), str(4 // lv)):
             monkeypatch.setenv("LMKAN_B200_RT", rt)
             Y = layers["1"].forward(Xd)
             assert _mixed(Y.cpu().numpy(), ref).max() <= TOL, (mode, rt)
