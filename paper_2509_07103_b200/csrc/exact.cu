@@ -33,14 +33,21 @@ namespace {
 
 constexpr int kExactWarps = 16;
 
-// rows per lane group: 32 at OT = 32 (a 512-row tile), 16 at OT = 16 / 8
-constexpr int exact_rt(int OT) { return OT == 32 ? 32 : 16; }
+// Outputs per lane: NRUN runs of 2 doubles (one LDS.128 each), the runs OT/2
+// apart: OT = 32 and 16 take 2 runs (8 / 4 lanes per row, 4 / 8 rows per
+// instruction), OT = 8 one run (4 lanes, 8 rows). A row's record (four fp64
+// weights + the node) is then shared by 4 lanes' worth of outputs, not 1:
+// shared-load wavefronts per coefficient 13/8 -> ~37/32 at OT = 32.
+constexpr int exact_nrun(int OT) { return OT >= 16 ? 2 : 1; }
+constexpr int exact_lpr(int OT) { return OT / (2 * exact_nrun(OT)); }  // lanes per row
+// rows per lane group: the register tile is RT rows x 2 NRUN doubles (32 doubles)
+constexpr int exact_rt(int OT) { return 16 / exact_nrun(OT); }
 
 struct ExactSmem {
     uint32_t sheet_bytes, off_recw, off_recn, off_thr, off_pts, off_bar, total;
 };
 __host__ __device__ inline ExactSmem exact_smem_layout(int G, int OT, bool gsheet) {
-    const int rows_w = (32 / OT) * exact_rt(OT);
+    const int rows_w = (32 / exact_lpr(OT)) * exact_rt(OT);
     ExactSmem s;
     s.sheet_bytes = (static_cast<uint32_t>((G + 1) * (G + 1)) * OT * 8u + 127u) & ~127u;
     uint32_t o = gsheet ? 0u : 2u * s.sheet_bytes;
@@ -64,7 +71,8 @@ template <int OT, typename XT, bool GSHEET>
 __global__ void __launch_bounds__(kExactWarps * 32, 1)
     exact_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
                  const double* __restrict__ table, int pairs, double gamma, const __grid_constant__ GridConst gc) {
-    constexpr int RT = exact_rt(OT), RPI = 32 / OT, ROWS_W = RPI * RT, LOC = (ROWS_W + 31) / 32;
+    constexpr int RT = exact_rt(OT), NRUN = exact_nrun(OT), LPR = exact_lpr(OT), RPI = 32 / LPR;
+    constexpr int ROWS_W = RPI * RT, LOC = (ROWS_W + 31) / 32;
     constexpr int R = kExactWarps * ROWS_W;
     extern __shared__ __align__(1024) unsigned char smem[];
     const int G = gc.G, nodes = (G + 1) * (G + 1);
@@ -102,13 +110,19 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
     __syncthreads();
 
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * R + warp * ROWS_W;
-    const int g = lane / OT, o = lane % OT;
-    const int col = ot * OT + o;
+    const int g = lane / LPR, c = lane % LPR;
+    // run r of the lane: doubles 2c + (r ^ flip) OT/2 of a node's OT. At OT = 16 a
+    // run is 64 B, on the bank half its index picks: odd lane groups take the runs
+    // in the order 1 0, so every LDS.128 puts half its rows on each half.
+    const int flip = (OT == 16 && NRUN == 2) ? (g & 1) : 0;
+    auto run_ofs = [&](int r) { return 2 * c + (r ^ flip) * (OT / 2); };
     double4* wrec = recw + warp * ROWS_W;
     int* nrec = recn + warp * ROWS_W;
-    double acc[RT];
+    double2 acc[RT][NRUN];
 #pragma unroll
-    for (int j = 0; j < RT; ++j) acc[j] = 0.0;
+    for (int j = 0; j < RT; ++j)
+#pragma unroll
+        for (int r = 0; r < NRUN; ++r) acc[j][r] = make_double2(0.0, 0.0);
 
     // x pair of the lane's rows, loaded one pair ahead (the loads are in flight
     // during the previous pair's gather)
@@ -160,18 +174,31 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
         for (int j = 0; j < RT; ++j) {
             const int q = j * RPI + g;
             const double4 w = wrec[q];
-            const double* b0 = sh + nrec[q] * OT + o;
+            const double* b0 = sh + nrec[q] * OT;
             const double* b1 = b0 + (G + 1) * OT;
-            double p00, p10, p01, p11;
-            if constexpr (GSHEET) {
-                p00 = __ldg(b0), p10 = __ldg(b1), p01 = __ldg(b0 + OT), p11 = __ldg(b1 + OT);
-            } else {
-                p00 = b0[0], p10 = b1[0], p01 = b0[OT], p11 = b1[OT];
+#pragma unroll
+            for (int r = 0; r < NRUN; ++r) {
+                const int o = run_ofs(r);
+                double2 p00, p10, p01, p11;
+                if constexpr (GSHEET) {
+                    p00 = __ldg(reinterpret_cast<const double2*>(b0 + o));
+                    p10 = __ldg(reinterpret_cast<const double2*>(b1 + o));
+                    p01 = __ldg(reinterpret_cast<const double2*>(b0 + OT + o));
+                    p11 = __ldg(reinterpret_cast<const double2*>(b1 + OT + o));
+                } else {
+                    p00 = *reinterpret_cast<const double2*>(b0 + o);
+                    p10 = *reinterpret_cast<const double2*>(b1 + o);
+                    p01 = *reinterpret_cast<const double2*>(b0 + OT + o);
+                    p11 = *reinterpret_cast<const double2*>(b1 + OT + o);
+                }
+                // y += ((w00 p00 + w10 p10) + w01 p01) + w11 p11, every op rounded (layer.hpp:129)
+                auto term = [&](double a, double b, double cc, double d) {
+                    return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w.x, a), __dmul_rn(w.y, b)), __dmul_rn(w.z, cc)),
+                                     __dmul_rn(w.w, d));
+                };
+                acc[j][r].x = __dadd_rn(acc[j][r].x, term(p00.x, p10.x, p01.x, p11.x));
+                acc[j][r].y = __dadd_rn(acc[j][r].y, term(p00.y, p10.y, p01.y, p11.y));
             }
-            const double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w.x, p00), __dmul_rn(w.y, p10)),
-                                                 __dmul_rn(w.z, p01)),
-                                       __dmul_rn(w.w, p11));
-            acc[j] = __dadd_rn(acc[j], t);
         }
         __syncthreads();  // every warp is done with buffer p & 1 and with its records
         if constexpr (!GSHEET) {
@@ -183,8 +210,14 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
     }
 #pragma unroll
     for (int j = 0; j < RT; ++j) {
-        const int64_t r = row0 + j * RPI + g;
-        if (r < rows && col < n_out) Y[r * n_out + col] = static_cast<XT>(__dmul_rn(acc[j], gamma));
+        const int64_t row = row0 + j * RPI + g;
+        if (row >= rows) continue;
+#pragma unroll
+        for (int r = 0; r < NRUN; ++r) {
+            const int col = ot * OT + run_ofs(r);
+            if (col < n_out) Y[row * n_out + col] = static_cast<XT>(__dmul_rn(acc[j][r].x, gamma));
+            if (col + 1 < n_out) Y[row * n_out + col + 1] = static_cast<XT>(__dmul_rn(acc[j][r].y, gamma));
+        }
     }
 }
 
@@ -222,7 +255,7 @@ unsigned blocks_for(size_t total) { return static_cast<unsigned>(std::min<size_t
 
 template <int OT, typename XT, bool GS>
 cudaError_t launch_exact_t(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
-    constexpr int R = kExactWarps * (32 / OT) * exact_rt(OT);
+    constexpr int R = kExactWarps * (32 / exact_lpr(OT)) * exact_rt(OT);
     auto kern = exact_kernel<OT, XT, GS>;
     const uint32_t smem = exact_smem_layout(L->G, OT, GS).total;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

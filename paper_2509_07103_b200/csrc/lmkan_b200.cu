@@ -1178,10 +1178,11 @@ int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int*
                     int* rows_per_cta_out, int* launches, int* mode, int* slabs, int* warps_per_cta) {
     if (!L) return fail(LMKAN_B200_EINVAL, "plan: null layer");
     if (L->exact) {  // mode 4: the reference-precision kernel (one launch, 16 warps per CTA)
+        const int nrun = L->OT >= 16 ? 2 : 1, lpr = L->OT / (2 * nrun), rt = 16 / nrun;  // exact.cu's geometry
         if (out_tile) *out_tile = L->OT;
-        if (rows_per_thread) *rows_per_thread = L->OT == 32 ? 32 : 16;
+        if (rows_per_thread) *rows_per_thread = rt;
         if (nbuf) *nbuf = L->exact_gsheet ? 0 : 2;
-        if (rows_per_cta_out) *rows_per_cta_out = 16 * (32 / L->OT) * (L->OT == 32 ? 32 : 16);
+        if (rows_per_cta_out) *rows_per_cta_out = 16 * (32 / lpr) * rt;
         if (launches) *launches = 1;
         if (mode) *mode = 4;
         if (slabs) *slabs = 1;
