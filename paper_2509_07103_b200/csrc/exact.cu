@@ -62,7 +62,7 @@ __host__ __device__ inline ExactSmem exact_smem_layout(int G, int OT, bool gshee
     o += static_cast<uint32_t>(G + 1) * 8u;
     o = (o + 15u) & ~15u;
     s.off_bar = o;
-    o += 16u;
+    o += 24u;  // two "landed" mbarriers + two finished-warp counters
     s.total = (o + 127u) & ~127u;
     return s;
 }
@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
     double* thr = reinterpret_cast<double*>(smem + Ls.off_thr);
     double* pts = reinterpret_cast<double*>(smem + Ls.off_pts);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Ls.off_bar);
+    unsigned* cnt = reinterpret_cast<unsigned*>(bar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int k = tid; k < gc.L; k += kExactWarps * 32) thr[k] = gc.t64[k];
     for (int k = tid; k <= G; k += kExactWarps * 32) pts[k] = gc.points[k];
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
         if (tid == 0) {
             mbar_init(&bar[0], 1);
             mbar_init(&bar[1], 1);
+            cnt[0] = cnt[1] = 0;
             fence_barrier_init();
             policy = policy_evict_last();
             issue(0);
@@ -138,7 +140,9 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
     };
     prefetch(0);
     for (int p = 0; p < pairs; ++p) {
-        // cells of the warp's rows for pair p (lane: rows q = k*32 + lane)
+        // cells of the warp's rows for pair p (lane: rows q = k*32 + lane); the
+        // warp-private records were last read by the previous pair's gather
+        __syncwarp();
 #pragma unroll
         for (int k = 0; k < LOC; ++k) {
             const int q = k * 32 + lane;
@@ -200,11 +204,17 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
                 acc[j][r].y = __dadd_rn(acc[j][r].y, term(p00.y, p10.y, p01.y, p11.y));
             }
         }
-        __syncthreads();  // every warp is done with buffer p & 1 and with its records
+        // slot release without a CTA barrier (as in fwd_fused_kernel): the last
+        // warp to finish with buffer p & 1 refills it with pair p + 2 (acq_rel
+        // counter: its own reads released, everyone else's acquired)
         if constexpr (!GSHEET) {
-            if (tid == 0 && p + 2 < pairs) {
-                fence_proxy_async();
-                issue(p + 2);
+            __syncwarp();
+            if (lane == 0 && atom_add_acq_rel_cta(&cnt[p & 1], 1u) == kExactWarps - 1) {
+                cnt[p & 1] = 0;
+                if (p + 2 < pairs) {
+                    fence_proxy_async();
+                    issue(p + 2);
+                }
             }
         }
     }
