@@ -40,21 +40,23 @@
 namespace lmkan_b200 {
 
 // Chunk boundaries over `total` units (rows or images): chunks of `full` units,
-// optionally tapered at both ends (full/4, full/2, full, ..., full, full/2,
-// full/4) so the first H2D and the last kernels + D2H, which nothing overlaps,
-// move less data. Tapering needs at least 2 full chunks' worth of units.
+// optionally tapered at both ends (levels = 2: full/4, full/2, full, ..., full,
+// full/2, full/4) so the first H2D and the last kernels + D2H, which nothing
+// overlaps, move less data. Tapering needs at least 2 full chunks' worth of units.
 struct ChunkSchedule {
     std::vector<int64_t> start;  // start[c] .. start[c + 1]
-    ChunkSchedule(int64_t total, int64_t full, bool taper) {
+    // levels: how many halvings taper each end (2: full/4, full/2, full, ...)
+    ChunkSchedule(int64_t total, int64_t full, int levels) {
         full = full < 1 ? 1 : full;
         std::vector<int64_t> sizes;
-        if (taper && full >= 4 && total >= 2 * full) {
-            const int64_t edge[2] = {full / 4, full / 2};
-            int64_t mid = total - 2 * (edge[0] + edge[1]);
-            sizes = {edge[0], edge[1]};
+        if (levels > 0 && full >= (int64_t(1) << levels) && total >= 2 * full) {
+            std::vector<int64_t> edge;
+            for (int l = levels; l >= 1; --l) edge.push_back(full >> l);
+            int64_t mid = total;
+            for (int64_t e : edge) mid -= 2 * e;
+            sizes = edge;
             for (; mid > 0; mid -= full) sizes.push_back(mid < full ? mid : full);
-            sizes.push_back(edge[1]);
-            sizes.push_back(edge[0]);
+            for (auto it = edge.rbegin(); it != edge.rend(); ++it) sizes.push_back(*it);
         } else {
             for (int64_t r = total; r > 0; r -= full) sizes.push_back(r < full ? r : full);
         }

@@ -692,7 +692,7 @@ int forward_host(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows) {
     const size_t y32_bytes = (static_cast<size_t>(chunk) * L->n_out * sizeof(float) + 255) & ~static_cast<size_t>(255);
     CK(P.reserve(static_cast<size_t>(chunk) * L->n_in * sizeof(XT),
                  static_cast<size_t>(chunk) * L->n_out * sizeof(XT) + (widen ? y32_bytes : 0)));
-    const ChunkSchedule cs(rows, chunk, env_int("LMKAN_B200_HOST_TAPER", 1) != 0);  // cfg2 e2e 3.51e6 -> 3.58e6
+    const ChunkSchedule cs(rows, chunk, env_int("LMKAN_B200_HOST_TAPER", 2));  // cfg2 e2e 3.51e6 -> 3.58e6 (2 levels vs none)
     return run_host_pipeline(
         P, cs.count(),
         [&](int64_t c, const void** h, size_t* b) {
@@ -1045,7 +1045,7 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
     const int chunk = static_cast<int>(std::min<int64_t>(N, std::max<int64_t>({(N + 7) / 8, min_imgs, 1})));
     const size_t in_img = static_cast<size_t>(H) * W * C, out_img = static_cast<size_t>(per_img) * L->n_out;
     CK(P.reserve(sizeof(float) * in_img * chunk, sizeof(float) * out_img * chunk));
-    const ChunkSchedule cs(N, chunk, env_int("LMKAN_B200_HOST_TAPER", 0) != 0);  // cfg4 e2e: tapering cost 15%
+    const ChunkSchedule cs(N, chunk, env_int("LMKAN_B200_HOST_TAPER", 0));  // cfg4 e2e: tapering cost 15%
     return run_host_pipeline(
         P, cs.count(),
         [&](int64_t c, const void** h, size_t* b) {
