@@ -197,3 +197,24 @@ def test_peer_access_checks(torch, pkg):
     pkg.peer_access(0, own)  # a device and itself: nothing to enable
     with pytest.raises(RuntimeError, match="not visible"):
         pkg.peer_access(0, "0000:ff:1f.7")
+
+
+def test_forward_dests_with_pair_blocks(torch, pkg, monkeypatch):
+    """Pair-block summation keeps its running sums in dests[0] (this GPU's own
+    buffer): every destination still receives the final columns, bitwise equal
+    to the plain forward, also across staged row chunks and tail rows."""
+    monkeypatch.setenv("LMKAN_B200_PAIR_BLOCK", "4")
+    n_in, n_out, G, rows = 96, 80, 12, 2999
+    ob, oe = 16, 64
+    for cap in (None, "1"):
+        if cap:
+            monkeypatch.setenv("LMKAN_B200_MAX_SCRATCH_MB", cap)  # forces row chunks
+        sl = pkg.Layer.random(n_in, n_out, G, seed=8, out_range=(ob, oe))
+        X = torch.randn((rows, n_in), device="cuda")
+        ref = sl.forward(X)
+        bufs = [torch.full((rows, n_out), float("nan"), device="cuda") for _ in range(3)]
+        sl.forward_dests(X, [b.data_ptr() for b in bufs], n_out, ob)
+        torch.cuda.synchronize()
+        for b in bufs:
+            assert torch.equal(b[:, ob:oe], ref)
+            assert torch.isnan(b[:, :ob]).all() and torch.isnan(b[:, oe:]).all()
