@@ -305,11 +305,20 @@ def main():
     import torch
     import paper_2509_07103_b200 as pkg
 
+    # LMKAN_B200_BENCH_SHARE_GPU=1: a plumbing dry run of the multi-rank paths
+    # on a box with fewer GPUs than ranks (ranks share devices, gloo instead of
+    # NCCL, which refuses two ranks on one GPU); never a measurement
+    share = os.environ.get("LMKAN_B200_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G = cfg["G"]
     B = cfg["batch"]
     out_sharded = bool(cfg.get("out_sharded"))
