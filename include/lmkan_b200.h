@@ -241,6 +241,9 @@ int lmkan_b200_plan(const lmkan_b200_layer* layer, int64_t rows, int* out_tile, 
 int lmkan_b200_lane_vectors(int out_tile);
 /* The same for a layer (duplicated-node OT = 16 tables use 2 runs of 32 B). */
 int lmkan_b200_layer_lane_vectors(const lmkan_b200_layer* layer);
+/* Output tiles per group of the gather grid's CTA order at `rows` rows (1: row
+ * tiles fastest; DRAM-traffic knob only, results do not depend on it); 0 on error. */
+int lmkan_b200_plan_cta_group(const lmkan_b200_layer* layer, int64_t rows);
 
 /* ---- training path ----
  *

@@ -360,6 +360,8 @@ class Layer:
             d["lane_vectors"] = int(lib.lmkan_b200_layer_lane_vectors(self._h))
         else:  # an older build under A/B (LMKAN_B200_LIB)
             d["lane_vectors"] = int(lib.lmkan_b200_lane_vectors(d["out_tile"]))
+        if hasattr(lib, "lmkan_b200_plan_cta_group"):
+            d["cta_group"] = int(lib.lmkan_b200_plan_cta_group(self._h, int(rows)))
         return d
 
     def close(self) -> None:

@@ -408,8 +408,32 @@ __global__ void __launch_bounds__(256) pixel_records_kernel(const XT* __restrict
     }
 }
 
+// CTA -> (row tile, output tile). The hardware dispatches CTAs in linear order
+// (x fastest); the linear index walks groups of `group` output tiles, and within
+// a group the output tiles fastest, then the row tiles. A wave of SMs then holds
+// ~num_sms / group row tiles x group output tiles, running in near lockstep over
+// the pairs, so L2 serves each pair's sheet to the wave's row tiles and each row
+// tile's records to its output tiles; DRAM reads per wave are (row tiles x
+// records) + (output tiles x sheets) instead of every row tile's records (group
+// 1: one output tile per wave, the round-1 order). The planner picks the group
+// (choose_cta_group: 1 by default, measured fastest); results do not depend on it.
+__device__ __forceinline__ void cta_tile(unsigned bx, unsigned by, unsigned gx, unsigned gy, int group,
+                                         int64_t& tile, int& ot) {
+    if (group <= 1) {
+        tile = bx;
+        ot = static_cast<int>(by);
+        return;
+    }
+    const unsigned lid = by * gx + bx, span = static_cast<unsigned>(group) * gx;
+    const unsigned grp = lid / span, rem = lid - grp * span;
+    const unsigned gs = min(static_cast<unsigned>(group), gy - grp * group);
+    ot = static_cast<int>(grp * group + rem % gs);
+    tile = rem / gs;
+}
+
 // K2/K3: gather-accumulate (with in-kernel locate in fused/global modes).
-// Grid: x = row tile (R rows), y = output tile (OT outputs). Table layout
+// Grid: x = row tile (R rows), y = output tile (OT outputs), remapped by
+// cta_tile. Table layout
 // [out_tile][pair][node][OT] fp32: one (out_tile, pair) sheet — or one slab of
 // it — is one contiguous bulk copy, and each node's OT outputs are a
 // contiguous, float4-aligned run.
@@ -446,7 +470,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
                      const float* __restrict__ table, int pairs, int nbuf, int S, float gamma,
                      const __grid_constant__ GridConst gc, const float2* __restrict__ recW,
                      const int* __restrict__ recO, int64_t rows_pad, const InputMap im, const EmitRecords emit,
-                     const __grid_constant__ GridConst gc_next, int Rt_arg, int pair_block) {
+                     const __grid_constant__ GridConst gc_next, int Rt_arg, int pair_block, int cta_group) {
     using Sh = FusedShape<OT, RT, NW, DUP>;
     constexpr int R = Sh::R;
     const int Rt = TAIL ? Rt_arg : R;  // full-tile kernels keep the row tile a compile-time constant
@@ -484,11 +508,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int vflip = V >= 2 ? (VSTEP == 16 ? (sub & 1) : ((sub >> 1) & 1)) : 0;
     auto vofs = [&](int v) { return (v ^ vflip) * VSTEP; };
     const int lane_base = 4 * c4 + (DUP ? (sub & 1) * OT : 0);  // DUP: odd lane groups read the second copy
-    const int64_t tile = blockIdx.x;
+    int64_t tile;
+    int ot;
+    cta_tile(blockIdx.x, blockIdx.y, gridDim.x, gridDim.y, cta_group, tile, ot);
     // row tiles of Rt <= R rows (Rt < R balances the grid over the SMs): lane
     // slots q >= Rt and rows >= rows are masked, issuing no gathers
     const int64_t row0 = tile * Rt;
-    const int ot = blockIdx.y;
     const float* tsrc = table + static_cast<size_t>(ot) * pairs * nodes * NS;
     const uint32_t sheet_floats = static_cast<uint32_t>(nodes) * NS;
     const uint32_t slab_floats = static_cast<uint32_t>(H) * (G + 1) * NS;  // slab stride within a sheet
@@ -651,20 +676,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
         // special registers, so nothing this rare path needs (row / column
         // indices, addresses) is hoisted out of the gather loop and kept live
         // in registers across it.
-        unsigned t_, bx_, by_;
+        unsigned t_, bx_, by_, gx_, gy_;
         asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t_));
         asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bx_));
         asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(by_));
+        asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(gx_));
+        asm volatile("mov.u32 %0, %%nctaid.y;" : "=r"(gy_));
+        int64_t tl_;
+        int ot_;
+        cta_tile(bx_, by_, gx_, gy_, cta_group, tl_, ot_);
         const int w_ = static_cast<int>(t_ >> 5), sb = static_cast<int>(t_ & 31) / Sh::LPR;
         const int vf = V >= 2 ? (VSTEP == 16 ? (sb & 1) : ((sb >> 1) & 1)) : 0;
-        const int cl = static_cast<int>(by_) * OT + 4 * (static_cast<int>(t_ & 31) % Sh::LPR);
+        const int cl = ot_ * OT + 4 * (static_cast<int>(t_ & 31) % Sh::LPR);
         const int64_t ld = out.ld;
         XT* const base = out.base[0] + out.col0;
         const bool vec = sizeof(XT) == 4 && (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (ld & 3) == 0;
         const bool live = !TAIL || w_ * Sh::ROWS_W < Rt;
 #pragma unroll
         for (int j = 0; j < RT; ++j) {
-            const int64_t r = static_cast<int64_t>(bx_) * Rt + w_ * Sh::ROWS_W + j * Sh::RPW + sb;
+            const int64_t r = tl_ * Rt + w_ * Sh::ROWS_W + j * Sh::RPW + sb;
             const bool row_ok = live && r < rows;
 #pragma unroll
             for (int v = 0; v < V; ++v) {

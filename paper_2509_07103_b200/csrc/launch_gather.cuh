@@ -25,7 +25,7 @@ cudaError_t launch_fused_t(const lmkan_b200_layer* L, const Plan& pl, const XT* 
     kern<<<grid, NW * 32, pl.smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table, L->pairs, pl.nbuf, pl.S,
                                            static_cast<float>(L->gamma), L->gc, recW, recO, pl.rows_pad, im, emit,
                                            emit.W ? *gc_next : L->gc, static_cast<int>(pl.row_tile),
-                                           Y.n > 0 ? L->pair_block : 0);
+                                           Y.n > 0 ? L->pair_block : 0, pl.cta_group);
     return cudaGetLastError();
 }
 

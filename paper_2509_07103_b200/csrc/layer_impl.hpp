@@ -46,6 +46,7 @@ struct Plan {
     int64_t row_tile;  // rows per CTA tile, <= sh.R (smaller to balance the grid over the SMs)
     int goff = 0;      // staged: node offsets read from global into registers (fwd_fused_kernel)
     int pix = 0;       // fused conv: records per image pixel (kModePixel), recO = the pixel records
+    int cta_group = 1; // output tiles per CTA-order group (cta_tile in gather.cuh; choose_cta_group)
 };
 
 // Launch the gather kernel variant selected by `pl` for output tile OT

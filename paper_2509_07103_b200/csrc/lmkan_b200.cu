@@ -150,6 +150,19 @@ int choose_pair_block(int pairs) {
     return b;
 }
 
+// CTA order of the gather grid (cta_tile, gather.cuh): g output tiles per
+// group; a wave of the SMs holds about num_sms / g row tiles x g output tiles.
+// Measured (same box, tools/ab_ctagroup.sh): g > 1 cuts K2's DRAM reads —
+// config 2 9.5 GB (g = 1) -> 6.4 (2) / 5.1 (4) / 6.1 (8), the config-5 shard
+// 199 -> 165 GB (2), 530 (16), 650 (64) — but is never faster: config 2
+// +0.06% at every g > 1, config 3 +0.6% at g = 4, config 5 +0.2% at g = 2 and
+// +4% / +11% / +15% at g = 7 / 16 / 64. The kernels are bound by the shared-
+// memory port with DRAM at 9-20% of its bandwidth, so the default stays the
+// fastest order (g = 1, row tiles fastest). LMKAN_B200_CTA_GROUP overrides.
+int choose_cta_group(const lmkan_b200_layer* L, const Plan&) {
+    return std::max(1, std::min(env_int("LMKAN_B200_CTA_GROUP", 1), L->n_ot));
+}
+
 // Mode: staged (K1 + K2) when several output tiles re-read the same cells (the
 // locate then runs once per (row, pair) instead of once per output tile and
 // the gather kernel's shared-memory port serves only gathers); fused (K3)
@@ -250,6 +263,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                         }
                         out = Plan{L->OT, RT, nbuf, mode, S, sh, s.total, nt, nt * Rt,
                                    mode == kModeStaged ? 2 : 1, Rt, goff};
+                        out.cta_group = choose_cta_group(L, out);
                         return true;
                     }
                 }
@@ -1172,6 +1186,14 @@ int lmkan_b200_lane_vectors(int out_tile) { return lane_vectors(out_tile); }
 int lmkan_b200_layer_lane_vectors(const lmkan_b200_layer* L) {
     if (!L) return fail(LMKAN_B200_EINVAL, "lane_vectors: null layer"), 0;
     return L->narrow || L->exact ? 1 : lane_vectors(L->OT, L->ns);
+}
+
+int lmkan_b200_plan_cta_group(const lmkan_b200_layer* L, int64_t rows) {
+    if (!L) return fail(LMKAN_B200_EINVAL, "plan_cta_group: null layer"), 0;
+    if (L->exact || L->narrow) return 1;
+    Plan pl;
+    if (!make_plan(L, rows, max_smem_optin(L->device), pl)) return fail(LMKAN_B200_EINVAL, "plan: no variant fits"), 0;
+    return pl.cta_group;
 }
 
 int lmkan_b200_plan(const lmkan_b200_layer* L, int64_t rows, int* out_tile, int* rows_per_thread, int* nbuf,

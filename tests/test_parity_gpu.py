@@ -622,3 +622,27 @@ def test_host_staging_paths_bitwise(torch, pkg, monkeypatch, x_pinned, y_pinned,
     layer.forward_host_ptr(Xh.data_ptr(), Yh.data_ptr(), rows, np.dtype(dtype).type)
     assert np.array_equal(Yh.numpy(), want)
     assert np.array_equal(layer.forward_host(Xh.numpy()), want)
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows,mode", [(64, 1024, 8, 5000, "staged"), (2304, 160, 4, 3000, "staged"),
+                                                     (64, 200, 8, 40000, "fused")])
+def test_cta_order_groups_bitwise(torch, pkg, oracle, monkeypatch, n_in, n_out, G, rows, mode):
+    """The gather grid's CTA order (cta_tile, LMKAN_B200_CTA_GROUP) changes
+    only which CTA runs which (row tile, output tile): every group size —
+    including a last, partial group and the pair-block fold (1152 pairs), which
+    re-derives its tile from the special registers — gives the same bits."""
+    rng = np.random.default_rng(n_in + n_out)
+    P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
+    layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
+    X = torch.randn((rows, n_in), device="cuda")
+    monkeypatch.setenv("LMKAN_B200_MODE", mode)
+    outs = []
+    for g in ("1", "3", "4", "64"):
+        monkeypatch.setenv("LMKAN_B200_CTA_GROUP", g)
+        p = layer.plan(rows)
+        assert p["mode"] == mode and p["cta_group"] == min(int(g), -(-n_out // p["out_tile"])), p
+        outs.append(layer.forward(X))
+    for y in outs[1:]:
+        assert torch.equal(y, outs[0])
+    ref = oracle.forward(G, P.astype(np.float64), X[:200].double().cpu().numpy(), 1.0)
+    assert _mixed(outs[0][:200].cpu().numpy(), ref).max() <= TOL
