@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -309,6 +310,33 @@ struct HostPipeline {
 // widen_out: the device result is fp32 while the caller's Y is fp64 (dst gives
 // the fp64 buffer and its byte count): the D2H moves the fp32 bytes (half) into
 // a pinned slot and the host pool widens them into Y.
+// LMKAN_B200_PIPE_TRACE=1: timing events around every chunk's H2D, kernels and
+// D2H, printed to stderr (ms from the first H2D) after the call — the timeline
+// a profiler would show, for tuning the chunking (not used otherwise).
+struct PipeTrace {
+    std::vector<cudaEvent_t> ev;  // per chunk: H2D begin / end, kernels begin / end, D2H begin / end
+    explicit PipeTrace(int64_t chunks) {
+        const char* e = std::getenv("LMKAN_B200_PIPE_TRACE");
+        if (!e || !std::atoi(e)) return;
+        ev.assign(static_cast<size_t>(chunks) * 6, nullptr);
+        for (auto& x : ev) cudaEventCreate(&x);
+    }
+    void mark(int64_t c, int k, cudaStream_t st) {
+        if (!ev.empty()) cudaEventRecord(ev[static_cast<size_t>(c) * 6 + k], st);
+    }
+    ~PipeTrace() {
+        if (ev.empty()) return;
+        const int64_t chunks = static_cast<int64_t>(ev.size()) / 6;
+        for (int64_t c = 0; c < chunks; ++c) {
+            float t[6] = {};
+            for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], ev[0], ev[static_cast<size_t>(c) * 6 + k]);
+            std::fprintf(stderr, "pipe chunk %lld: h2d %.4f-%.4f  kern %.4f-%.4f  d2h %.4f-%.4f ms\n",
+                         static_cast<long long>(c), t[0], t[1], t[2], t[3], t[4], t[5]);
+        }
+        for (auto x : ev) cudaEventDestroy(x);
+    }
+};
+
 template <class Src, class Dst, class Compute, class Fail>
 int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute compute, Fail cuda_fail,
                       bool widen_out = false) {
@@ -367,6 +395,7 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
             P.pool.copy(hd, P.hY[c % S], yb);
         return 0;
     };
+    PipeTrace tr(chunks);
     for (int64_t c = 0; c < chunks && rc == 0; ++c) {
         const int b = static_cast<int>(c % S);
         const void* hs = nullptr;
@@ -386,7 +415,9 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
         }
         if (stage_out) hd = P.hY[b];  // chunk c - S was drained from it at iteration c - 1
         if (c >= S) e = cudaStreamWaitEvent(P.in, P.kdone[b], 0);  // chunk c - S has consumed dX[b]
+        tr.mark(c, 0, P.in);
         if (e == cudaSuccess) e = cudaMemcpyAsync(P.dX[b], hs, xb, cudaMemcpyHostToDevice, P.in);
+        tr.mark(c, 1, P.in);
         if (e == cudaSuccess) e = cudaEventRecord(P.h2d[b], P.in);
         cudaStream_t comp = P.comp[c & 1];
         if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, P.h2d[b], 0);
@@ -395,11 +426,15 @@ int run_host_pipeline(HostPipeline& P, int64_t chunks, Src src, Dst dst, Compute
             rc = cuda_fail(e, "host pipeline: H2D");
             break;
         }
+        tr.mark(c, 2, comp);
         rc = compute(c, P.dX[b], P.dY[b], comp);
         if (rc) break;
+        tr.mark(c, 3, comp);
         e = cudaEventRecord(P.kdone[b], comp);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(P.out, P.kdone[b], 0);
+        tr.mark(c, 4, P.out);
         if (e == cudaSuccess) e = cudaMemcpyAsync(hd, P.dY[b], yb / yscale, cudaMemcpyDeviceToHost, P.out);
+        tr.mark(c, 5, P.out);
         if (e == cudaSuccess) e = cudaEventRecord(P.d2h[b], P.out);
         if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline: D2H");
         // drain two chunks behind, so the GPU always has chunks c-1 and c queued
