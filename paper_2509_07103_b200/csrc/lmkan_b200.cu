@@ -210,8 +210,11 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                     const int RT = A / lane_vectors(L->OT, L->ns);
                     if (force_rt && RT != force_rt) continue;
                     if (mode == kModeGlobal && A != kRTChoices[2]) continue;  // the global-sheet kernel is built for RT2 only
-                    // warps per CTA: 16, or for batches too small to give every SM a
-                    // 16-warp CTA at RT = 4, the largest of {8, 4, 2, 1} that does
+                    // warps per CTA: 16, or for batches too small to give half the
+                    // SMs a 16-warp CTA at RT = 4, the largest of {8, 4, 2, 1} that
+                    // does. (Not all SMs: conv stage 3's 16384 rows ran 0.307 ms as
+                    // 128 CTAs of 16 warps and 0.423 ms as 256 of 8 — 1.7 waves of
+                    // CTAs that each still stream every sheet.)
                     int NW = kWarps;
                     if (A == kRTChoices[2] && S == 1 && mode != kModeGlobal) {
                         const int force_nw = env_int("LMKAN_B200_NW", 0);
@@ -219,7 +222,7 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
                             NW = force_nw;
                         } else {
                             while (NW > 1 && ((rows + shape_rt(L->OT, RT, NW, NSt).R - 1) / shape_rt(L->OT, RT, NW, NSt).R) *
-                                                     L->n_ot < L->num_sms)
+                                                     L->n_ot * 2 < L->num_sms)
                                 NW >>= 1;
                         }
                     }
