@@ -52,7 +52,9 @@ def update_ncu():
                             ("cfg3_head", "cfg3_head_narrow", None),
                             ("cfg4_gather", "cfg4_gather_K3_pixel", "cfg4"),
                             ("cfg1_gather", "cfg1_gather", "cfg1"),
-                            ("cfg5_gather", "cfg5_shard_gather", "cfg5")]:
+                            ("cfg5_gather", "cfg5_shard_gather", "cfg5"),
+                            ("cfg6_gather", "cfg6_conv_stage2_gather", "cfg6"),
+                            ("cfg7_gather", "cfg7_conv_stage3_gather", "cfg7")]:
         rep = os.path.join(SRC, cap + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -83,11 +85,12 @@ def main():
         for f in os.listdir(prof):
             shutil.copy(os.path.join(prof, f), os.path.join(DST, f))
     update_ncu()  # no-op unless .ncu-rep files are present locally
-    for name in [f"bench_cfg{c}" for c in (1, 2, 3, 4, 5)] + ["bench_cfg2_exact", "bench_reference_cfg2"]:
+    for name in ([f"bench_cfg{c}" for c in (1, 2, 3, 4, 5, 6, 7)] + ["bench_cfg2_exact"] +
+                 [f"bench_reference_cfg{c}" for c in (1, 2, 3, 4, 6, 7)]):
         line = last_json(os.path.join(SRC, name + ".json"))
         if line:
             open(os.path.join(DST, f"{R}_{name}.json"), "w").write(line + "\n")
-    for c in (1, 2, 3, 4, 5):
+    for c in (1, 2, 3, 4, 5, 6, 7):
         p = os.path.join(SRC, f"launches_cfg{c}.csv")
         if os.path.exists(p):
             shutil.copy(p, os.path.join(DST, f"{R}_cfg{c}_launches.csv"))
