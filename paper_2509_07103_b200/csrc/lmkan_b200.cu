@@ -104,19 +104,37 @@ int env_int(const char* name, int dflt) {
 // else the narrowest single-buffered. Unslabbed wins over wider: a slabbed
 // sheet makes every row issue (predicated-off) loads in every slab (measured at
 // G = 28: OT 32 unslabbed 7.0 ms, OT 16 8.6 ms, OT 32 two slabs 11.2 ms).
+// Before that (G >= 12): the widest double-buffered unslabbed OT that still
+// gives >= 3 output tiles, so the planner stages the cells (K1 locates each
+// (row, pair) once for every output tile, K2 only gathers) instead of fusing
+// the locate into one or two wide tiles. Measured (tools/ot_sweep.sh, same
+// box), n_out = 64 as four OT = 16 tiles vs the wide tile: 576→64 G=16 262144
+// rows 3.57 → 3.31 ms, 65536 rows 0.82 → 0.76, conv stage 3 0.307 → 0.283;
+// 128→64 G=28 2^20 rows 3.40 (OT 32) → 3.06, 65536 rows 0.244 → 0.226; but
+// 64→64 G=8 (81-node sheets, a cheap fused locate) 16384 rows 0.041 → 0.043
+// and config 1's step +2.4%, hence G >= 12. n_out = 128 keeps OT = 32 (4.86 ms
+// vs 5.67 at OT 16), n_out = 32 OT = 32 (fused; 0.27 vs 0.35 ms at OT 16).
+bool out_tile_fits(int OT, int G, int want_buf, int S, int smem_cap) {
+    for (int A : kRTChoices) {
+        // (global offsets: the tallest tile, unslabbed, only; see make_plan)
+        const FusedSmem s = fused_smem_layout(G, OT, A / lane_vectors(OT), want_buf, kModeStaged, S, kWarps, 0,
+                                              A == kRTChoices[0] && S == 1 ? 1 : 0);
+        if (static_cast<int>(s.total) <= smem_cap) return true;
+    }
+    return false;
+}
+
 int choose_out_tile(int n_out, int G, int smem_cap) {
     const int v = env_int("LMKAN_B200_OT", 0);
     if (v == 16 || v == 32 || v == 64) return v;
+    if (G >= 12)
+        for (int OT : {64, 32, 16})
+            if ((n_out + OT - 1) / OT >= 3 && out_tile_fits(OT, G, 2, 1, smem_cap)) return OT;
     for (int want_buf : {2, 1}) {
         for (int S = 1; S <= (want_buf == 2 ? 3 : 1); ++S) {
             for (int OT : {64, 32, 16}) {
                 if (OT > 16 && OT / 2 >= n_out) continue;
-                for (int A : kRTChoices) {
-                    // (global offsets: the tallest tile, unslabbed, only; see make_plan)
-                    const FusedSmem s = fused_smem_layout(G, OT, A / lane_vectors(OT), want_buf, kModeStaged, S,
-                                                          kWarps, 0, A == kRTChoices[0] && S == 1 ? 1 : 0);
-                    if (static_cast<int>(s.total) <= smem_cap) return OT;
-                }
+                if (out_tile_fits(OT, G, want_buf, S, smem_cap)) return OT;
             }
         }
     }

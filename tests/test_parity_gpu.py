@@ -571,6 +571,7 @@ def test_balanced_tiles_lane_runs_bitwise(torch, pkg, oracle, monkeypatch, n_in,
     as the full tiles and meet the parity bar."""
     rng = np.random.default_rng(rows + n_out)
     P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
+    monkeypatch.setenv("LMKAN_B200_OT", str(n_out))  # one n_out-wide tile: V = n_out / 16 runs per lane
     layer = pkg.Layer.from_host(n_in, n_out, G, P.astype(np.float64), 1.0)
     X = torch.randn((rows, n_in), device="cuda")
     monkeypatch.setenv("LMKAN_B200_MODE", mode)
@@ -590,17 +591,20 @@ def test_output_slices_across_table_layouts_bitwise(torch, pkg):
     tiles with 4 float4 runs per lane, 32-wide with 2, 16-wide duplicated-node
     tables); every slice equals the matching columns of the full layer, bit for
     bit, and its table reads back exactly."""
-    n_in, n_out, G, rows = 40, 112, 12, 6000
+    n_in, n_out, G, rows = 40, 304, 12, 6000
     rng = np.random.default_rng(40)
     P = (rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)).astype(np.float32)
     Pd = torch.from_numpy(P).cuda()
     X = torch.randn((rows, n_in), device="cuda")
     full = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0)
     Y = full.forward(X)
-    for ob, oe in [(0, 16), (16, 48), (48, 112), (100, 112)]:
+    widths = set()
+    for ob, oe in [(0, 16), (16, 48), (48, 112), (112, 304), (100, 112)]:
         sl = pkg.Layer.from_device(n_in, n_out, G, Pd, 1.0, out_range=(ob, oe))
+        widths.add(sl.out_tile)
         assert torch.equal(sl.forward(X), Y[:, ob:oe]), (ob, oe, sl.out_tile)
         np.testing.assert_array_equal(sl.read_table(), P[..., ob:oe].astype(np.float64))
+    assert widths == {16, 32, 64}, widths
 
 
 @pytest.mark.parametrize("x_pinned,y_pinned", [(False, False), (True, False), (False, True), (True, True)])
