@@ -650,3 +650,23 @@ def test_cta_order_groups_bitwise(torch, pkg, oracle, monkeypatch, n_in, n_out, 
         assert torch.equal(y, outs[0])
     ref = oracle.forward(G, P.astype(np.float64), X[:200].double().cpu().numpy(), 1.0)
     assert _mixed(outs[0][:200].cpu().numpy(), ref).max() <= TOL
+
+
+@pytest.mark.parametrize("n_in,n_out,G,rows,ot,mode", [
+    (576, 64, 16, 16384, 16, "staged"),    # conv stage 3: four OT = 16 tiles, cells staged once
+    (128, 64, 28, 65536, 16, "staged"),
+    (64, 64, 8, 1024, 64, "staged"),       # config 1: G < 12 keeps the one wide tile
+    (288, 32, 16, 65536, 32, "fused"),     # two tiles at most: the single fused tile
+    (1024, 1024, 16, 65536, 64, "staged"),  # config 2
+    (128, 128, 28, 65536, 32, "staged"),   # config 3 layer 2
+])
+def test_output_tile_choice(torch, pkg, oracle, n_in, n_out, G, rows, ot, mode):
+    """choose_out_tile: with G >= 12 the widest tile that still gives >= 3
+    output tiles (the planner then stages the cells), else the widest that
+    double-buffers; the chosen layout meets the parity bar."""
+    layer = pkg.Layer.random(n_in, n_out, G, seed=3)
+    p = layer.plan(rows)
+    assert (layer.out_tile, p["mode"]) == (ot, mode), p
+    X = torch.randn((min(rows, 4096), n_in), device="cuda")
+    ref = oracle.forward(G, layer.read_table(), X[:64].double().cpu().numpy(), 1.0)
+    assert _mixed(layer.forward(X)[:64].cpu().numpy(), ref).max() <= TOL
