@@ -417,6 +417,26 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
         }
         plx.pix = 1;
         recO = reinterpret_cast<int*>(pixrec);
+        // Ring depth vs L1: the gather reads the pixel records through L1 (each
+        // is reused by up to k^2 patch rows), and L1 gets what the sheet ring
+        // leaves of the SM's 256 KB. When the CTA's records fit beside a
+        // shallower ring (>= 2 slots), take the deepest ring that leaves them
+        // room — conv stage 2: 6 slots 0.276 ms at a 3.6% L1 hit rate, 2 slots
+        // 0.271 ms at 74% (ncu) — else keep the deepest (cfg4: 259 KB of
+        // records per CTA fit no L1; 5 slots beat 2 by 2.4%).
+        if (!env_int("LMKAN_B200_NBUF", 0) && env_int("LMKAN_B200_PIX_L1", 1)) {
+            const double px_per_row = static_cast<double>(im.H) * im.W / (static_cast<double>(im.out_h) * im.out_w);
+            const double foot = static_cast<double>(plx.row_tile) * px_per_row * (im.C / 2) * sizeof(int4);
+            constexpr double kL1Smem = 256.0 * 1024;  // unified L1 / shared memory per SM
+            for (int nb = plx.nbuf; nb >= 2; --nb) {
+                const FusedSmem fs = fused_smem_layout(L->G, L->OT, plx.RT, nb, plx.mode, plx.S, plx.sh.NW, L->ns);
+                if (foot <= kL1Smem - fs.total) {
+                    plx.nbuf = nb;
+                    plx.smem = fs.total;
+                    break;
+                }
+            }
+        }
     }
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
