@@ -80,3 +80,9 @@ torch.cuda.synchronize()
 print("records", int(i1.sum()), int(i2.sum()))
 lh = pkg.Layer.random(96, 80, 12, seed=9)
 print("host staging", float(np.abs(lh.forward_host(np.random.default_rng(1).standard_normal((20000, 96)))).sum()))
+# round 2, late: CTA-order groups (cta_tile, incl. the pair-block fold's
+# re-derived tile) and the pixel-record conv with its L1-capped ring
+run({"LMKAN_B200_CTA_GROUP": "2"}, 256, 192, 16, 1500)
+run({"LMKAN_B200_CTA_GROUP": "3", "LMKAN_B200_PAIR_BLOCK": "4"}, 40, 80, 12, 900)
+lay = pkg.Layer.random(9 * 32, 32, 16, seed=7)
+print("conv stage 2", float(lay.conv_forward(torch.randn((256, 18, 18, 32), device="cuda"), 3, 1).abs().sum()))
