@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
                 if (r < rows) {
                     const double x1 = static_cast<double>(xa[k]);
                     const double x2 = static_cast<double>(xb[k]);
-                    const int i1 = cell_index<double>(x1, thr, gc.L), i2 = cell_index<double>(x2, thr, gc.L);
+                    // the estimate-then-verify index (locate.cuh): the same cell as the
+                    // exact search for every input, at one MUFU + two threshold loads
+                    const int i1 = cell_index_fast<double>(x1, thr, G, gc.L);
+                    const int i2 = cell_index_fast<double>(x2, thr, G, gc.L);
                     const double a = __dsub_rn(pts[i1 + 1], x1), b = __dsub_rn(x1, pts[i1]);
                     const double c = __dsub_rn(pts[i2 + 1], x2), d = __dsub_rn(x2, pts[i2]);
                     const double inv = __ldg(gc.inv_areas + i1 * G + i2);
