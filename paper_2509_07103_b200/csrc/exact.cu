@@ -17,11 +17,13 @@
 // whose sheet double-buffers in shared memory); per pair the (G+1)^2 x OT
 // sheet arrives by bulk copy (cp.async.bulk + mbarrier, two buffers, a CTA
 // barrier per pair). A warp locates the cells of its rows into a warp-private
-// record slice (fp64 weights), then every lane gathers one output of 32 / OT
+// record slice (fp64 weights) — or, with several output tiles, loads them from
+// exact_records_kernel's staged records (launch_exact) — then every lane gathers one output of 32 / OT
 // rows per instruction: LDS.64 of a 256-B (OT = 32) or 128-B (OT = 16) run is
 // 2 wavefronts with no bank conflicts. Sheets too large for shared memory
 // (G > ~40) are read from L2 directly.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/lmkan_b200.h"
@@ -67,10 +69,37 @@ __host__ __device__ inline ExactSmem exact_smem_layout(int G, int OT, bool gshee
     return s;
 }
 
-template <int OT, typename XT, bool GSHEET>
+// Cell records of the staged variant, [pair][rows]: the four fp64 weights and
+// the node, computed exactly as the fused kernel's locate below (so Y is the
+// same bits either way). One thread per (row, pair), rows fastest: a pair's
+// stores are contiguous, and the x loads of consecutive pairs share sectors
+// that L2 still holds.
+template <typename XT>
+__global__ void exact_records_kernel(const XT* __restrict__ X, int64_t rows, int n_in,
+                                     const __grid_constant__ GridConst gc, double4* __restrict__ W,
+                                     int* __restrict__ N) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (r >= rows) return;
+    const int G = gc.G;
+    const double x1 = static_cast<double>(__ldg(X + r * n_in + 2 * p));
+    const double x2 = static_cast<double>(__ldg(X + r * n_in + 2 * p + 1));
+    const int i1 = cell_index_fast<double>(x1, gc.t64, G, gc.L);
+    const int i2 = cell_index_fast<double>(x2, gc.t64, G, gc.L);
+    const double a = __dsub_rn(__ldg(gc.points + i1 + 1), x1), b = __dsub_rn(x1, __ldg(gc.points + i1));
+    const double c = __dsub_rn(__ldg(gc.points + i2 + 1), x2), d = __dsub_rn(x2, __ldg(gc.points + i2));
+    const double inv = __ldg(gc.inv_areas + i1 * G + i2);
+    const size_t k = static_cast<size_t>(p) * rows + r;
+    W[k] = make_double4(__dmul_rn(__dmul_rn(a, c), inv), __dmul_rn(__dmul_rn(b, c), inv),
+                        __dmul_rn(__dmul_rn(a, d), inv), __dmul_rn(__dmul_rn(b, d), inv));
+    N[k] = i1 * (G + 1) + i2;
+}
+
+template <int OT, typename XT, bool GSHEET, bool STAGED>
 __global__ void __launch_bounds__(kExactWarps * 32, 1)
     exact_kernel(const XT* __restrict__ X, XT* __restrict__ Y, int64_t rows, int n_in, int n_out,
-                 const double* __restrict__ table, int pairs, double gamma, const __grid_constant__ GridConst gc) {
+                 const double* __restrict__ table, int pairs, double gamma, const __grid_constant__ GridConst gc,
+                 const double4* __restrict__ recW, const int* __restrict__ recN) {
     constexpr int RT = exact_rt(OT), NRUN = exact_nrun(OT), LPR = exact_lpr(OT), RPI = 32 / LPR;
     constexpr int ROWS_W = RPI * RT, LOC = (ROWS_W + 31) / 32;
     constexpr int R = kExactWarps * ROWS_W;
@@ -126,16 +155,26 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
 #pragma unroll
         for (int r = 0; r < NRUN; ++r) acc[j][r] = make_double2(0.0, 0.0);
 
-    // x pair of the lane's rows, loaded one pair ahead (the loads are in flight
-    // during the previous pair's gather)
+    // x pair (staged: the cell record) of the lane's rows, loaded one pair ahead
+    // (the loads are in flight during the previous pair's gather)
     XT xa[LOC], xb[LOC];
+    double4 pw[LOC];
+    int pn[LOC];
     auto prefetch = [&](int p) {
 #pragma unroll
         for (int k = 0; k < LOC; ++k) {
             const int64_t r = row0 + k * 32 + lane;
             const bool ok = k * 32 + lane < ROWS_W && r < rows;
-            xa[k] = ok ? __ldg(X + r * n_in + 2 * p) : XT(0);
-            xb[k] = ok ? __ldg(X + r * n_in + 2 * p + 1) : XT(0);
+            if constexpr (STAGED) {
+                const size_t i = static_cast<size_t>(p) * rows + r;
+                const double2* q = reinterpret_cast<const double2*>(recW + (ok ? i : 0));
+                const double2 lo = ok ? __ldg(q) : make_double2(0.0, 0.0), hi = ok ? __ldg(q + 1) : make_double2(0.0, 0.0);
+                pw[k] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                pn[k] = ok ? __ldg(recN + i) : 0;
+            } else {
+                xa[k] = ok ? __ldg(X + r * n_in + 2 * p) : XT(0);
+                xb[k] = ok ? __ldg(X + r * n_in + 2 * p + 1) : XT(0);
+            }
         }
     };
     prefetch(0);
@@ -150,7 +189,10 @@ __global__ void __launch_bounds__(kExactWarps * 32, 1)
                 const int64_t r = row0 + q;
                 double4 w = make_double4(0.0, 0.0, 0.0, 0.0);
                 int node = 0;
-                if (r < rows) {
+                if constexpr (STAGED) {
+                    w = pw[k];
+                    node = pn[k];
+                } else if (r < rows) {
                     const double x1 = static_cast<double>(xa[k]);
                     const double x2 = static_cast<double>(xb[k]);
                     // the estimate-then-verify index (locate.cuh): the same cell as the
@@ -266,27 +308,68 @@ __global__ void export64_kernel(const double* __restrict__ table, double* __rest
 
 unsigned blocks_for(size_t total) { return static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 64)); }
 
-template <int OT, typename XT, bool GS>
-cudaError_t launch_exact_t(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+template <int OT, typename XT, bool GS, bool STAGED>
+cudaError_t launch_exact_t(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, const double4* W,
+                           const int* N, cudaStream_t st) {
     constexpr int R = kExactWarps * (32 / exact_lpr(OT)) * exact_rt(OT);
-    auto kern = exact_kernel<OT, XT, GS>;
+    auto kern = exact_kernel<OT, XT, GS, STAGED>;
     const uint32_t smem = exact_smem_layout(L->G, OT, GS).total;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int64_t tiles = (rows + R - 1) / R;
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(L->n_ot));
-    kern<<<grid, kExactWarps * 32, smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table64, L->pairs, L->gamma, L->gc);
+    kern<<<grid, kExactWarps * 32, smem, st>>>(X, Y, rows, L->n_in, L->n_out, L->table64, L->pairs, L->gamma, L->gc,
+                                                W, N);
     return cudaGetLastError();
 }
 
-template <typename XT>
-cudaError_t launch_exact(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+template <typename XT, bool STAGED>
+cudaError_t launch_exact_k(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, const double4* W,
+                           const int* N, cudaStream_t st) {
     const bool gs = L->exact_gsheet;
     switch (L->OT) {
-        case 32: return gs ? launch_exact_t<32, XT, true>(L, X, Y, rows, st) : launch_exact_t<32, XT, false>(L, X, Y, rows, st);
-        case 16: return gs ? launch_exact_t<16, XT, true>(L, X, Y, rows, st) : launch_exact_t<16, XT, false>(L, X, Y, rows, st);
-        default: return gs ? launch_exact_t<8, XT, true>(L, X, Y, rows, st) : launch_exact_t<8, XT, false>(L, X, Y, rows, st);
+        case 32: return gs ? launch_exact_t<32, XT, true, STAGED>(L, X, Y, rows, W, N, st)
+                           : launch_exact_t<32, XT, false, STAGED>(L, X, Y, rows, W, N, st);
+        case 16: return gs ? launch_exact_t<16, XT, true, STAGED>(L, X, Y, rows, W, N, st)
+                           : launch_exact_t<16, XT, false, STAGED>(L, X, Y, rows, W, N, st);
+        default: return gs ? launch_exact_t<8, XT, true, STAGED>(L, X, Y, rows, W, N, st)
+                           : launch_exact_t<8, XT, false, STAGED>(L, X, Y, rows, W, N, st);
     }
+}
+
+// Staged when several output tiles would otherwise each redo the fp64 locate
+// of every (row, pair) (the locate is ~24% of the fused kernel's time at cfg2's
+// 32 tiles: a timing-only build without it ran 38.9 vs 51.4 ms): K1 writes the
+// records once (36 B per (row, pair), row chunks under the scratch cap), the
+// gather kernel prefetches them a pair ahead. LMKAN_B200_EXACT_STAGED=0 keeps
+// the fused kernel.
+template <typename XT>
+cudaError_t launch_exact(const lmkan_b200_layer* L, const XT* X, XT* Y, int64_t rows, cudaStream_t st) {
+    const char* env = std::getenv("LMKAN_B200_EXACT_STAGED");
+    if (L->n_ot < 2 || L->pairs > 65535 || (env && !std::atoi(env)))
+        return launch_exact_k<XT, false>(L, X, Y, rows, nullptr, nullptr, st);
+    const char* cap_env = std::getenv("LMKAN_B200_MAX_SCRATCH_MB");
+    const size_t cap = static_cast<size_t>(cap_env ? std::atoi(cap_env) : 4096) << 20;
+    const size_t per_row = static_cast<size_t>(L->pairs) * (sizeof(double4) + sizeof(int));
+    const int64_t chunk = std::max<int64_t>(1024, static_cast<int64_t>(cap / per_row));
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+        const int64_t n = std::min(chunk, rows - r0);
+        double4* W = nullptr;
+        int* N = nullptr;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&W), static_cast<size_t>(n) * L->pairs * sizeof(double4), st);
+        if (e != cudaSuccess) return e;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&N), static_cast<size_t>(n) * L->pairs * sizeof(int), st);
+        if (e == cudaSuccess) {
+            exact_records_kernel<XT><<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(L->pairs)),
+                                       256, 0, st>>>(X + r0 * L->n_in, n, L->n_in, L->gc, W, N);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = launch_exact_k<XT, true>(L, X + r0 * L->n_in, Y + r0 * L->n_out, n, W, N, st);
+        if (N) cudaFreeAsync(N, st);
+        cudaFreeAsync(W, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace

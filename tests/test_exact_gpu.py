@@ -64,3 +64,23 @@ def test_exact_layer_refusals(torch, pkg):
         layer.records(X, "in_kernel")
     with pytest.raises(ValueError, match="reference-precision"):
         pkg.Model.from_layers([layer])
+
+
+def test_exact_staged_records_and_row_chunks(torch, pkg, oracle, monkeypatch):
+    """Layers with several output tiles stage the fp64 cell records (one
+    locate per (row, pair) instead of one per output tile); the staged path,
+    its row chunks under a small scratch cap, and the fused kernel all give
+    the reference's bits."""
+    n_in, n_out, G, rows = 40, 96, 12, 5000
+    rng = np.random.default_rng(11)
+    P = rng.standard_normal((G + 1, G + 1, n_in // 2, n_out)) / np.sqrt(n_in // 2)
+    X = rng.standard_normal((rows, n_in)) * 1.5
+    layer = pkg.Layer.from_host(n_in, n_out, G, P, 1.0, precision=64)
+    ref = oracle.forward(G, P, X, 1.0)
+    Xd = torch.from_numpy(X).cuda()
+    for env in ({}, {"LMKAN_B200_MAX_SCRATCH_MB": "1"}, {"LMKAN_B200_EXACT_STAGED": "0"}):
+        for k in ("LMKAN_B200_MAX_SCRATCH_MB", "LMKAN_B200_EXACT_STAGED"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _assert_bits(layer.forward(Xd).cpu().numpy(), ref)
