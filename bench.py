@@ -556,6 +556,9 @@ def main():
         balg_row = sum(2 * b_alg(a, b) for a, b in cfg["layers"])
     achieved = B * balg_row / (kernel_ms / 1e3) / 1e9
     plan = layers[0].plan(B)
+    if conv and hasattr(layers[0], "conv_plan"):  # the conv call's own plan (pixel records, L1-capped ring)
+        cp = layers[0].conv_plan(conv["N"], conv["H"], conv["W"], conv["C"], conv["k"], conv["s"])
+        plan.update(nbuf=cp["nbuf"], rows_per_cta=cp["rows_per_cta"], pixel_records=cp["pixel_records"])
     cpu = None
     if not args.no_cpu_baseline and ws == 1 and args.precision == 32:
         if out_sharded:  # 146 GB fp64 table does not fit the host: time a 16-output slice, scale by cost ~ n_out

@@ -244,6 +244,11 @@ int lmkan_b200_layer_lane_vectors(const lmkan_b200_layer* layer);
 /* Output tiles per group of the gather grid's CTA order at `rows` rows (1: row
  * tiles fastest; DRAM-traffic knob only, results do not depend on it); 0 on error. */
 int lmkan_b200_plan_cta_group(const lmkan_b200_layer* layer, int64_t rows);
+/* Plan of an implicit-im2col conv call (lmkan_b200_conv_forward_*): the sheet
+ * ring depth the gather kernel runs with (after the pixel-record L1 cap), its
+ * rows per CTA, and whether cells are located once per image pixel. */
+int lmkan_b200_conv_plan(const lmkan_b200_layer* layer, int N, int H, int W, int C, int k, int s, int* nbuf,
+                         int* rows_per_cta, int* pixel_records);
 
 /* ---- training path ----
  *

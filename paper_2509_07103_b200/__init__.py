@@ -364,6 +364,13 @@ class Layer:
             d["cta_group"] = int(lib.lmkan_b200_plan_cta_group(self._h, int(rows)))
         return d
 
+    def conv_plan(self, N: int, H: int, W: int, Cc: int, k: int, s: int) -> dict:
+        """Ring depth, rows per CTA and pixel-record use of a conv_forward call."""
+        v = [C.c_int() for _ in range(3)]
+        check(lib.lmkan_b200_conv_plan(self._h, int(N), int(H), int(W), int(Cc), int(k), int(s),
+                                       *[C.byref(x) for x in v]))
+        return {"nbuf": v[0].value, "rows_per_cta": v[1].value, "pixel_records": bool(v[2].value)}
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             if getattr(self, "_owned", True):
@@ -512,6 +519,13 @@ class Model:
     def infer_host_ptr(self, X_ptr: int, Y_ptr: int, rows: int, dtype=np.float32) -> None:
         fn = lib.lmkan_b200_model_infer_host_f32 if dtype == np.float32 else lib.lmkan_b200_model_infer_host_f64
         check(fn(self._h, C.c_void_p(X_ptr), C.c_void_p(Y_ptr), int(rows), 0))
+
+    def conv_plan(self, N: int, H: int, W: int, Cc: int, k: int, s: int) -> dict:
+        """Ring depth, rows per CTA and pixel-record use of a conv_forward call."""
+        v = [C.c_int() for _ in range(3)]
+        check(lib.lmkan_b200_conv_plan(self._h, int(N), int(H), int(W), int(Cc), int(k), int(s),
+                                       *[C.byref(x) for x in v]))
+        return {"nbuf": v[0].value, "rows_per_cta": v[1].value, "pixel_records": bool(v[2].value)}
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -61,6 +61,7 @@ _SIGS = [
     ("lmkan_b200_lane_vectors", C.c_int, [C.c_int]),
     ("lmkan_b200_layer_lane_vectors", C.c_int, [_P]),
     ("lmkan_b200_plan_cta_group", C.c_int, [_P, C.c_int64]),
+    ("lmkan_b200_conv_plan", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P]),
     ("lmkan_b200_backward_f64", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int64, C.c_uint64, _P]),
     ("lmkan_b200_backward_workers", C.c_int64, [_P, C.c_int64]),
     ("lmkan_b200_backward_host_f64", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int64, C.c_size_t]),

@@ -296,6 +296,33 @@ bool make_plan(const lmkan_b200_layer* L, int64_t rows, int smem_cap, Plan& out,
 
 // Cap on the stream-ordered cell-record scratch of the staged mode; larger
 // batches are processed in row chunks (LMKAN_B200_MAX_SCRATCH_MB overrides).
+// implicit-im2col conv in the fused mode: records per image pixel (kModePixel)
+bool pixel_eligible(const Plan& pl, const InputMap& im) {
+    return pl.mode == kModeFused && pl.S == 1 && im.conv && im.C % 2 == 0 && im.npix > 0 &&
+           im.npix < (int64_t(1) << 31) && env_int("LMKAN_B200_PIXREC", 1);
+}
+
+// Ring depth vs L1: the gather reads the pixel records through L1 (each is
+// reused by up to k^2 patch rows), and L1 gets what the sheet ring leaves of
+// the SM's 256 KB. When the CTA's records fit beside a shallower ring (>= 2
+// slots), take the deepest ring that leaves them room — conv stage 2: 6 slots
+// 0.276 ms at a 3.6% L1 hit rate, 2 slots 0.271 ms at 74% (ncu) — else keep
+// the deepest (cfg4: 259 KB of records per CTA fit no L1; 5 slots beat 2 by 2.4%).
+void pixel_ring_cap(const lmkan_b200_layer* L, const InputMap& im, Plan& plx) {
+    if (env_int("LMKAN_B200_NBUF", 0) || !env_int("LMKAN_B200_PIX_L1", 1)) return;
+    const double px_per_row = static_cast<double>(im.H) * im.W / (static_cast<double>(im.out_h) * im.out_w);
+    const double foot = static_cast<double>(plx.row_tile) * px_per_row * (im.C / 2) * sizeof(int4);
+    constexpr double kL1Smem = 256.0 * 1024;  // unified L1 / shared memory per SM
+    for (int nb = plx.nbuf; nb >= 2; --nb) {
+        const FusedSmem fs = fused_smem_layout(L->G, L->OT, plx.RT, nb, plx.mode, plx.S, plx.sh.NW, L->ns);
+        if (foot <= kL1Smem - fs.total) {
+            plx.nbuf = nb;
+            plx.smem = fs.total;
+            return;
+        }
+    }
+}
+
 size_t record_scratch_cap() { return static_cast<size_t>(env_int("LMKAN_B200_MAX_SCRATCH_MB", 4096)) << 20; }
 
 // One launch group (K1 + K2 in staged mode, K3 otherwise) over `rows` rows.
@@ -402,8 +429,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
     // gather fetch the records through the im2col map (kModePixel)
     Plan plx = pl;
     int4* pixrec = nullptr;
-    if (pl.mode == kModeFused && pl.S == 1 && im.conv && im.C % 2 == 0 && im.npix > 0 &&
-        im.npix < (int64_t(1) << 31) && !link.emit.W && env_int("LMKAN_B200_PIXREC", 1)) {
+    if (pixel_eligible(pl, im) && !link.emit.W) {
         const int64_t nrec = im.npix * (im.C / 2);
         CK(cudaMallocAsync(reinterpret_cast<void**>(&pixrec), static_cast<size_t>(nrec) * sizeof(int4), st));
         // one wave of 8 blocks per SM, grid-stride: each block stages the grid
@@ -417,26 +443,7 @@ int forward_rows(const lmkan_b200_layer* L, const Plan& pl, const XT* X, const O
         }
         plx.pix = 1;
         recO = reinterpret_cast<int*>(pixrec);
-        // Ring depth vs L1: the gather reads the pixel records through L1 (each
-        // is reused by up to k^2 patch rows), and L1 gets what the sheet ring
-        // leaves of the SM's 256 KB. When the CTA's records fit beside a
-        // shallower ring (>= 2 slots), take the deepest ring that leaves them
-        // room — conv stage 2: 6 slots 0.276 ms at a 3.6% L1 hit rate, 2 slots
-        // 0.271 ms at 74% (ncu) — else keep the deepest (cfg4: 259 KB of
-        // records per CTA fit no L1; 5 slots beat 2 by 2.4%).
-        if (!env_int("LMKAN_B200_NBUF", 0) && env_int("LMKAN_B200_PIX_L1", 1)) {
-            const double px_per_row = static_cast<double>(im.H) * im.W / (static_cast<double>(im.out_h) * im.out_w);
-            const double foot = static_cast<double>(plx.row_tile) * px_per_row * (im.C / 2) * sizeof(int4);
-            constexpr double kL1Smem = 256.0 * 1024;  // unified L1 / shared memory per SM
-            for (int nb = plx.nbuf; nb >= 2; --nb) {
-                const FusedSmem fs = fused_smem_layout(L->G, L->OT, plx.RT, nb, plx.mode, plx.S, plx.sh.NW, L->ns);
-                if (foot <= kL1Smem - fs.total) {
-                    plx.nbuf = nb;
-                    plx.smem = fs.total;
-                    break;
-                }
-            }
-        }
+        pixel_ring_cap(L, im, plx);
     }
     cudaError_t e;
     if (ev_begin) cudaEventRecord(ev_begin, st);
@@ -1118,6 +1125,22 @@ int lmkan_b200_conv_forward_host_f32(const lmkan_b200_layer* L, const float* img
                                          per_img * cs.size(c), st, nullptr, nullptr, imc);
         },
         [](cudaError_t e, const char* what) { return cuda_fail(e, what); });
+}
+
+int lmkan_b200_conv_plan(const lmkan_b200_layer* L, int N, int H, int W, int C, int k, int s, int* nbuf,
+                         int* rows_per_cta, int* pixel_records) {
+    InputMap im;
+    if (int rc = conv_map(L, N, H, W, C, k, s, im)) return rc;
+    Plan pl;
+    const int64_t rows = static_cast<int64_t>(N) * im.out_h * im.out_w;
+    if (!make_plan(L, std::max<int64_t>(rows, 1), max_smem_optin(L->device), pl))
+        return fail(LMKAN_B200_EINVAL, "conv_plan: no kernel variant fits shared memory");
+    const bool pix = pixel_eligible(pl, im);
+    if (pix) pixel_ring_cap(L, im, pl);
+    if (nbuf) *nbuf = pl.nbuf;
+    if (rows_per_cta) *rows_per_cta = static_cast<int>(pl.row_tile > 0 ? pl.row_tile : pl.sh.R);
+    if (pixel_records) *pixel_records = pix ? 1 : 0;
+    return LMKAN_B200_OK;
 }
 
 int lmkan_b200_conv_forward_f32(const lmkan_b200_layer* L, const float* img, int N, int H, int W, int C, int k,

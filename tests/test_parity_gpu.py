@@ -670,3 +670,15 @@ def test_output_tile_choice(torch, pkg, oracle, n_in, n_out, G, rows, ot, mode):
     X = torch.randn((min(rows, 4096), n_in), device="cuda")
     ref = oracle.forward(G, layer.read_table(), X[:64].double().cpu().numpy(), 1.0)
     assert _mixed(layer.forward(X)[:64].cpu().numpy(), ref).max() <= TOL
+
+
+def test_conv_plan_pixel_ring(torch, pkg):
+    """lmkan_b200_conv_plan: pixel records for even channel counts in the fused
+    mode; the sheet ring is capped only when the CTA's pixel records then fit
+    the L1 it leaves (conv stage 2), not when they fit no L1 (config 4)."""
+    s2 = pkg.Layer.random(288, 32, 16, seed=1).conv_plan(256, 18, 18, 32, 3, 1)
+    c4 = pkg.Layer.random(144, 16, 16, seed=1).conv_plan(256, 34, 34, 16, 3, 1)
+    assert s2["pixel_records"] and c4["pixel_records"], (s2, c4)
+    assert s2["nbuf"] == 2 and c4["nbuf"] >= 4, (s2, c4)
+    with pytest.raises(ValueError):
+        pkg.Layer.random(144, 16, 16, seed=1).conv_plan(2, 2, 2, 16, 3, 1)  # kernel larger than the image
